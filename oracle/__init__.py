@@ -1,0 +1,226 @@
+"""TEST INFRASTRUCTURE ONLY -- the CPU oracle for the loop hafnian with repeated rows/columns.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product
+(``paper_2108_01622_b200``) never imports it, and this package never imports the
+product: the two share no code ("Oracle").
+
+The arithmetic lives in ``oracle.c`` (x87 long double, OpenMP).  This module is a thin
+ctypes marshaller plus ``build()``.  Every function cites the paper passage it follows
+(``P:nnn`` = line of PAPER.md of arXiv 2108.01622).
+
+Parity status per function:
+  lhaf_brute        pinned: telephone numbers, (N-1)!!, 2x2 closed form, rank-one, TMSV,
+                    coherent, involution counts          (tests/test_oracle_pins.py)
+  lhaf_et           pinned: agreement with lhaf_brute (N <= 12) + closed forms to N = 40
+  matched_reps      pinned: the paper's worked example n = (2,1,0,3) -> 6 terms
+  fds_term          pinned: 2x2 closed form; full-sum agreement with lhaf_brute/lhaf_et
+  lhaf_fds          pinned: agreement with lhaf_brute / lhaf_et, closed forms
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so with gcc (-O2 -fopenmp, long double)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(
+            ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"]
+        )
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        dp = ctypes.POINTER(ctypes.c_double)
+        ip = ctypes.POINTER(ctypes.c_int32)
+        lib.orc_expand.argtypes = [dp, dp, ip, ctypes.c_int32, dp]
+        lib.orc_expand.restype = ctypes.c_int
+        lib.orc_lhaf_brute.argtypes = [ctypes.c_int32, dp, dp]
+        lib.orc_lhaf_brute.restype = None
+        lib.orc_count_matchings.argtypes = [ctypes.c_int32]
+        lib.orc_count_matchings.restype = ctypes.c_uint64
+        lib.orc_lhaf_et.argtypes = [ctypes.c_int32, dp, dp, dp]
+        lib.orc_lhaf_et.restype = None
+        lib.orc_matched_reps.argtypes = [ip, ctypes.c_int32, ip, ip, ip, ctypes.c_int32, ip]
+        lib.orc_matched_reps.restype = ctypes.c_int32
+        lib.orc_fds_term.argtypes = [ctypes.c_int32, dp, dp, ip, ctypes.c_int32, dp]
+        lib.orc_fds_term.restype = None
+        lib.orc_lhaf_fds.argtypes = [dp, dp, ip, ctypes.c_int32, ctypes.c_int32, dp, dp]
+        lib.orc_lhaf_fds.restype = ctypes.c_uint64
+        _lib = lib
+    return _lib
+
+
+def _cplx(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _iptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def expand(A, gamma, reps) -> np.ndarray:
+    """A_n: repeat row/col i reps[i] times, diagonal replaced by gamma_n."""
+    A = _cplx(A)
+    gamma = _cplx(gamma)
+    reps = np.ascontiguousarray(np.asarray(reps, dtype=np.int32))
+    k = reps.shape[0]
+    N = int(reps.sum())
+    out = np.zeros((N, N), dtype=np.complex128)
+    _load().orc_expand(_dptr(A), _dptr(gamma), _iptr(reps), k, _dptr(out))
+    return out
+
+
+def lhaf_brute(Ahat) -> complex:
+    """Sum over single-pair matchings of the (already expanded) matrix."""
+    Ahat = _cplx(Ahat)
+    N = Ahat.shape[0]
+    out = np.zeros(2)
+    _load().orc_lhaf_brute(N, _dptr(Ahat), _dptr(out))
+    return complex(out[0], out[1])
+
+
+def count_matchings(N: int) -> int:
+    """Number of single-pair matchings the brute force visits (telephone number T(N))."""
+    return int(_load().orc_count_matchings(N))
+
+
+def lhaf_et(Ahat) -> complex:
+    """Eigenvalue-trace inclusion/exclusion, Eq. ET_loop/ET_poly, explicit powers."""
+    return lhaf_et_kappa(Ahat)[0]
+
+
+def lhaf_et_kappa(Ahat):
+    """(value, sum_Z |f(A_Z)|): the second number over |value| is the cancellation factor
+    kappa; the oracle's rounding error is bounded by ~ kappa * 5.4e-20 * (small factor)."""
+    Ahat = _cplx(Ahat)
+    N = Ahat.shape[0]
+    out = np.zeros(2)
+    sabs = np.zeros(1)
+    _load().orc_lhaf_et(N, _dptr(Ahat), _dptr(out), _dptr(sabs))
+    return complex(out[0], out[1]), float(sabs[0])
+
+
+EPS_LD = 2.0 ** -64   # unit roundoff of x87 long double
+
+
+def lhaf(A, gamma, reps, method: str = "auto") -> complex:
+    """lhaf of the expanded matrix A_n: brute force for N <= 14, else ET."""
+    Ahat = expand(A, gamma, reps)
+    N = Ahat.shape[0]
+    if method == "brute" or (method == "auto" and N <= 14):
+        return lhaf_brute(Ahat)
+    return lhaf_et(Ahat)
+
+
+def lhaf_mixed(A2, gamma2, reps) -> complex:
+    """Mixed-state lhaf: A2 (2k x 2k) expanded with the doubled pattern (reps, reps)."""
+    reps = np.asarray(reps, dtype=np.int32)
+    return lhaf(A2, gamma2, np.concatenate([reps, reps]))
+
+
+def matched_reps(reps):
+    """Greedy pair matching. Returns (pairs [(p,q)], eta [..], leftover or None)."""
+    reps = np.ascontiguousarray(np.asarray(reps, dtype=np.int32))
+    k = reps.shape[0]
+    cap = max(1, int(reps.sum()))
+    p = np.zeros(cap, np.int32)
+    q = np.zeros(cap, np.int32)
+    eta = np.zeros(cap, np.int32)
+    left = np.zeros(1, np.int32)
+    H = _load().orc_matched_reps(_iptr(reps), k, _iptr(p), _iptr(q), _iptr(eta), cap, _iptr(left))
+    if H < 0:
+        raise RuntimeError("matched_reps capacity exceeded")
+    pairs = [(int(p[i]), int(q[i])) for i in range(H)]
+    return pairs, [int(e) for e in eta[:H]], (int(left[0]) if left[0] >= 0 else None)
+
+
+def fds_term(C, v, w, n: int) -> complex:
+    """One repeated-pair sieve term g(w), explicit powers."""
+    C = _cplx(C)
+    v = _cplx(v)
+    w = np.ascontiguousarray(np.asarray(w, dtype=np.int32))
+    h = w.shape[0]
+    assert C.shape == (2 * h, 2 * h) and v.shape == (2 * h,)
+    out = np.zeros(2)
+    _load().orc_fds_term(h, _dptr(C), _dptr(v), _iptr(w), n, _dptr(out))
+    return complex(out[0], out[1])
+
+
+def lhaf_fds(A, gamma, reps, mixed: bool = False):
+    """Full repeated-pair sieve, no halving. Returns (value, T, sum|term| 2^-n)."""
+    A = _cplx(A)
+    gamma = _cplx(gamma)
+    reps = np.ascontiguousarray(np.asarray(reps, dtype=np.int32))
+    out = np.zeros(2)
+    sabs = np.zeros(1)
+    T = _load().orc_lhaf_fds(_dptr(A), _dptr(gamma), _iptr(reps), reps.shape[0], int(mixed),
+                             _dptr(out), _dptr(sabs))
+    return complex(out[0], out[1]), int(T), float(sabs[0])
+
+
+def reduced_system(A, gamma, reps, mixed: bool = False):
+    """Oracle-side reduced matrix for per-term parity: (C, v, eta, n) following reading C8
+    (index list (p_1..p_H, q_1..q_H), C_ab = A_{r_a r_b} incl. diagonal, v = gamma_r,
+    phantom row/col zero with loop 1).  Pure Python indexing, no arithmetic."""
+    A = _cplx(A)
+    gamma = _cplx(gamma)
+    reps = np.asarray(reps, dtype=np.int32)
+    if mixed:
+        k = reps.shape[0]
+        pairs = [(i, i + k) for i in range(k) if reps[i] > 0]
+        eta = [int(reps[i]) for i in range(k) if reps[i] > 0]
+        left = None
+    else:
+        pairs, eta, left = matched_reps(reps)
+    r = [p for p, _ in pairs]
+    s = [q for _, q in pairs]
+    if left is not None:
+        r.append(left)
+        s.append(-1)
+        eta = eta + [1]
+    idx = r + s
+    d = len(idx)
+    C = np.zeros((d, d), np.complex128)
+    v = np.zeros(d, np.complex128)
+    for a in range(d):
+        v[a] = 1.0 if idx[a] < 0 else gamma[idx[a]]
+        for b in range(d):
+            if idx[a] >= 0 and idx[b] >= 0:
+                C[a, b] = A[idx[a], idx[b]]
+    return C, v, eta, int(sum(eta))
+
+
+def decode(t: int, eta):
+    """Mixed-radix decode of term index t (lowest pair fastest): digits k_h, w = eta - 2k,
+    sign (-1)^{sum k}, weight prod C(eta_h, k_h) (reading C5).  Integers only."""
+    from math import comb
+    ks = []
+    rem = int(t)
+    for e in eta:
+        ks.append(rem % (e + 1))
+        rem //= e + 1
+    w = [e - 2 * kk for e, kk in zip(eta, ks)]
+    sign = -1 if sum(ks) % 2 else 1
+    weight = 1
+    for e, kk in zip(eta, ks):
+        weight *= comb(e, kk)
+    return ks, w, sign, weight
