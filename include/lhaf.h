@@ -1,0 +1,177 @@
+/*
+ * lhaf.h -- C-ABI of the B200 loop-hafnian library for matrices with repeated rows/columns
+ * (photon collisions at number-resolving detectors), after Bulmer et al., "The Boundary for
+ * Quantum Advantage in Gaussian Boson Sampling", arXiv 2108.01622.
+ *
+ * Citations "P:nnn" are lines of the paper text; "S8(a) a4" etc. are rows of the
+ * hot-path scope table in SURVEY.md.
+ *
+ * What is computed.  For a symmetric complex k x k matrix A, loop weights gamma (k) and a
+ * photon pattern reps (k non-negative integers, N = sum reps), lhaf_rpt returns lhaf(A_n),
+ * the loop hafnian (sum over single-pair matchings) of the N x N matrix A_n
+ * formed by repeating row/column i of A reps[i] times and replacing the diagonal by the
+ * correspondingly repeated gamma.  The method is the finite-difference sieve
+ * over the repeated pairs of the greedy matching:
+ *     lhaf = 2^{1-n} sum_{t < floor(T/2)} (-1)^{sum k} prod_h C(eta_h, k_h) g(eta - 2k)
+ * (readings C5/C6 of DESIGN.md), one per-term evaluation g per mixed-radix index t.
+ *
+ * Conventions shared by every entry point.
+ *  - Complex numbers are interleaved (re, im) IEEE doubles; matrices are row-major.
+ *  - Host pointers unless the name ends in _dev.  The caller owns every buffer; the library
+ *    copies what it needs and keeps no pointer after the call returns.  Outputs are written
+ *    only when the call returns LHAF_OK.
+ *  - A's diagonal is the weight of pairing two photons detected in the same mode (it is used
+ *    only when some reps[i] >= 2); gamma holds the loop weights (reading C8).  A caller that
+ *    holds an already-expanded matrix with the loops on its diagonal passes reps = 1 and
+ *    gamma = its diagonal.
+ *  - Errors are returned as lhaf_status, never thrown across the ABI; lhaf_last_error()
+ *    gives a message for the calling thread's last non-OK status.
+ *  - Calls are serialised internally (one device context per process); results are
+ *    bit-identical for any number of ranks (fixed chunking + ordered double-double sums).
+ *  - All arithmetic runs on the GPU (sm_100a kernels); there is no CPU fallback.  Without a
+ *    usable CUDA device every compute call returns LHAF_E_CUDA.
+ */
+#ifndef LHAF_H_
+#define LHAF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LHAF_OK = 0,
+  LHAF_E_ARG = 1,           /* null pointer, k < 0 or > LHAF_MAX_MODES, negative reps, batch < 0 */
+  LHAF_E_NOT_SYMMETRIC = 2, /* max|A - A^T| > 1e-12 * max(1, max|A|) */
+  LHAF_E_TOO_LARGE = 3,     /* reduced dimension d > LHAF_MAX_DIM, degree n > LHAF_MAX_DEGREE,
+                               or term count above the guard */
+  LHAF_E_CUDA = 4,          /* CUDA runtime failure, or no device */
+  LHAF_E_NCCL = 5,          /* NCCL failure (multi-rank only) */
+  LHAF_E_STATE = 6          /* library not initialised as required / inconsistent ranks */
+} lhaf_status;
+
+#define LHAF_MAX_MODES 4096
+#define LHAF_MAX_DIM 64       /* d = 2H (H = number of distinct pairs incl. the phantom) */
+#define LHAF_MAX_DEGREE 128   /* n = sum eta (lambda degree) */
+#define LHAF_MAX_PAIRS 64
+
+/* Host-only plan of one pattern (S8(a) a2-a4).  Greedy matching of P:474-481 (reading C9:
+ * stable sort by (count desc, mode asc) every round, n2 := 0 when one mode remains), the
+ * phantom pair for odd N (reading C7), and the term counts.  mixed != 0 selects the natural
+ * pairing (i, i+k) x reps_i of P:425-428 (reading C11). */
+typedef struct {
+  int32_t N;            /* photons = sum reps */
+  int32_t H;            /* distinct pairs incl. phantom */
+  int32_t d;            /* reduced dimension 2H */
+  int32_t n;            /* lambda degree = sum eta */
+  int32_t leftover;     /* mode of the odd leftover photon, or -1 */
+  int32_t pad_;
+  uint64_t T;           /* prod (eta_h + 1): full sieve term count */
+  uint64_t T_eval;      /* floor(T/2): evaluated terms after halving (reading C6) */
+  int32_t p[LHAF_MAX_PAIRS];   /* pair h = (p[h], q[h]); q = -1 for the phantom */
+  int32_t q[LHAF_MAX_PAIRS];
+  int32_t eta[LHAF_MAX_PAIRS];
+} lhaf_plan_info;
+
+/* Plan only (no GPU).  reps: k int32, k in [0, LHAF_MAX_MODES].  For mixed, reps has length
+ * k and refers to a 2k-mode matrix.  Returns LHAF_E_ARG on bad input, LHAF_E_TOO_LARGE when
+ * H exceeds LHAF_MAX_PAIRS. */
+lhaf_status lhaf_plan(const int32_t *reps, int32_t k, int32_t mixed, lhaf_plan_info *info);
+
+/* Mixed-radix decode of term index t for a plan (S8(a) a4, integers only, bit-exact):
+ * digits k_h in [0, eta_h] with pair 0 fastest, w_h = eta_h - 2 k_h, sign = (-1)^{sum k},
+ * weight = prod C(eta_h, k_h) (exact integer if < 2^64; returned as uint64).  k_out, w_out
+ * have room for info->H entries. */
+lhaf_status lhaf_decode(const lhaf_plan_info *info, uint64_t t, int32_t *k_out, int32_t *w_out,
+                        int32_t *sign_out, uint64_t *weight_out);
+
+/* One loop hafnian (S8(a) a1-a12).  A: k*k c128, gamma: k c128, reps: k int32.  out[2] =
+ * (re, im) of lhaf(A_n).  N = 0 gives (1, 0).  Errors: E_ARG, E_NOT_SYMMETRIC, E_TOO_LARGE,
+ * E_CUDA, E_NCCL.  After lhaf_init_rank(nranks > 1) the term range is sharded over the ranks
+ * and every rank receives the full result (one NCCL all-reduce of chunk partials). */
+lhaf_status lhaf_rpt(const double *A, const double *gamma, const int32_t *reps, int32_t k,
+                     double out[2]);
+
+/* Batch of loop hafnians sharing A (S8(a) a14; the chain-rule use of P:371-373).
+ * gamma: k c128 when gamma_stride == 0 (shared), else batch rows of gamma_stride (>= k)
+ * c128 each.  reps: batch*k int32 row-major.  out: batch*2 doubles.  Patterns are sharded
+ * over ranks by contiguous blocks of work units. */
+lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_stride,
+                           const int32_t *reps, int32_t k, int32_t batch, double *out);
+
+/* Mixed-state loop hafnian (S8(a) a13): lhaf of the 2N x 2N A_n formed from the 2k x 2k
+ * matrix A2 by repeating rows/cols i and i+k reps[i] times, evaluated with the
+ * natural pairing (i, i+k) x reps_i.  A2: 2k*2k c128, gamma2: 2k c128,
+ * reps: k int32. */
+lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t *reps,
+                           int32_t k, double out[2]);
+
+/* Same three entry points with DEVICE pointers for A / gamma / out (reps stays on the host,
+ * since planning is host integer work) and an explicit cudaStream_t (passed as void*; NULL =
+ * the legacy default stream).  The call is asynchronous with respect to the host only in the
+ * sense that results land in out_dev on `stream`; it synchronises the stream before return. */
+lhaf_status lhaf_rpt_batch_dev(const double *A_dev, const double *gamma_dev, int64_t gamma_stride,
+                               const int32_t *reps, int32_t k, int32_t batch, int32_t mixed,
+                               double *out_dev, void *stream);
+
+/* ---- Jobs: a planned, device-resident evaluation (for timing and multi-rank control) ----
+ * lhaf_job_create plans and uploads a batch (mixed != 0: natural pairing over A2 / gamma2,
+ * each reps row of length k).  lhaf_job_run evaluates work units [unit_begin, unit_end) into
+ * the job's chunk-partial array (zeroed by lhaf_job_reset); lhaf_job_finalize sums the
+ * partials in chunk order (double-double) and writes batch*2 doubles to out (host pointer if
+ * out_is_device == 0).  One work unit = a fixed, rank-independent chunk of one pattern's
+ * terms; units of a pattern are contiguous. */
+typedef struct lhaf_job lhaf_job;
+typedef struct {
+  int32_t batch;
+  int32_t d_max;
+  int32_t n_max;
+  int32_t kernel;        /* kernel variant id selected for this job */
+  uint64_t units;        /* total work units */
+  uint64_t terms;        /* total evaluated terms (sum of T_eval) */
+  double flops_per_term_model; /* algorithmic FP64 flops per term of the selected kernel */
+} lhaf_job_info;
+
+lhaf_status lhaf_job_create(const double *A, const double *gamma, int64_t gamma_stride,
+                            const int32_t *reps, int32_t k, int32_t batch, int32_t mixed,
+                            int32_t A_is_device, lhaf_job **job);
+lhaf_status lhaf_job_info_get(const lhaf_job *job, lhaf_job_info *info);
+lhaf_status lhaf_job_reset(lhaf_job *job, void *stream);
+lhaf_status lhaf_job_run(lhaf_job *job, uint64_t unit_begin, uint64_t unit_end, void *stream);
+/* All-reduce (sum) of the partial array over the ranks of lhaf_init_rank (no-op if 1 rank). */
+lhaf_status lhaf_job_allreduce(lhaf_job *job, void *stream);
+lhaf_status lhaf_job_finalize(lhaf_job *job, double *out, int32_t out_is_device, void *stream);
+/* Optional diagnostic: per-pattern sum_t |term_t| * 2^{1-n} (the conditioning denominator:
+ * kappa = abs_sum / |lhaf|).  Valid after lhaf_job_finalize.  out: batch doubles (host). */
+lhaf_status lhaf_job_abs_sum(lhaf_job *job, double *out);
+/* Device pointer and byte size of the partial array (for external all-reduce). */
+lhaf_status lhaf_job_partials(lhaf_job *job, void **dev_ptr, size_t *bytes);
+void lhaf_job_destroy(lhaf_job *job);
+
+/* Per-term diagnostic (S8(c) pin P14): g(t) for nt sampled term indices of pattern 0 of the
+ * job, computed by the same device code as the sieve.  g_out: nt*2 doubles (host). */
+lhaf_status lhaf_job_terms(lhaf_job *job, const uint64_t *t, int32_t nt, double *g_out);
+
+/* ---- Devices and ranks ---- */
+/* Select the CUDA device of this process (default 0, or LHAF_DEVICE env). */
+lhaf_status lhaf_set_device(int32_t device);
+/* Multi-rank (one process per GPU).  Rank 0 calls lhaf_get_unique_id and broadcasts the 128
+ * bytes (e.g. through torch.distributed); every rank then calls lhaf_init_rank.  NCCL is
+ * loaded at run time (dlopen of libnccl.so.2). */
+lhaf_status lhaf_get_unique_id(void *id128);
+lhaf_status lhaf_init_rank(int32_t rank, int32_t nranks, const void *id128, int32_t device);
+lhaf_status lhaf_rank_info(int32_t *rank, int32_t *nranks);
+
+/* Kernel override for experiments: 0 = automatic, else a variant id. */
+lhaf_status lhaf_set_kernel(int32_t variant);
+
+const char *lhaf_last_error(void);
+const char *lhaf_version(void);
+void lhaf_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LHAF_H_ */

@@ -1,0 +1,289 @@
+"""paper_2108_01622_b200 -- B200 (sm_100a) loop hafnians with repeated rows/columns.
+
+Thin ctypes binding over the C-ABI of ``include/lhaf.h`` (liblhaf.so, built in-tree by
+``paper_2108_01622_b200.build``).  Argument marshalling only: every step of the method runs
+in the library's CUDA kernels.  There is no CPU fallback: if liblhaf.so is missing, importing
+the binding raises, and without a CUDA device every compute call raises ``LhafError``.
+
+Names follow the C-ABI: ``lhaf_rpt``, ``lhaf_rpt_batch``, ``lhaf_rpt_mixed``,
+``lhaf_rpt_batch_dev``, ``lhaf_plan``, ``lhaf_decode``, the ``Job`` wrapper over
+``lhaf_job_*``, and the rank calls ``lhaf_get_unique_id`` / ``lhaf_init_rank``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblhaf.so")
+
+LHAF_MAX_PAIRS = 64
+LHAF_OK = 0
+_STATUS = {0: "LHAF_OK", 1: "LHAF_E_ARG", 2: "LHAF_E_NOT_SYMMETRIC", 3: "LHAF_E_TOO_LARGE",
+           4: "LHAF_E_CUDA", 5: "LHAF_E_NCCL", 6: "LHAF_E_STATE"}
+
+
+class LhafError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("H", ctypes.c_int32), ("d", ctypes.c_int32),
+                ("n", ctypes.c_int32), ("leftover", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("T", ctypes.c_uint64), ("T_eval", ctypes.c_uint64),
+                ("p", ctypes.c_int32 * LHAF_MAX_PAIRS), ("q", ctypes.c_int32 * LHAF_MAX_PAIRS),
+                ("eta", ctypes.c_int32 * LHAF_MAX_PAIRS)]
+
+    def pairs(self):
+        return [(self.p[h], self.q[h]) for h in range(self.H)]
+
+    def etas(self):
+        return [self.eta[h] for h in range(self.H)]
+
+
+class JobInfo(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("d_max", ctypes.c_int32), ("n_max", ctypes.c_int32),
+                ("kernel", ctypes.c_int32), ("units", ctypes.c_uint64), ("terms", ctypes.c_uint64),
+                ("flops_per_term_model", ctypes.c_double)]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2108_01622_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    dp = ctypes.POINTER(ctypes.c_double)
+    ip = ctypes.POINTER(ctypes.c_int32)
+    vp = ctypes.c_void_p
+    u64 = ctypes.c_uint64
+    sig = {
+        "lhaf_plan": ([ip, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(PlanInfo)]),
+        "lhaf_decode": ([ctypes.POINTER(PlanInfo), u64, ip, ip, ip, ctypes.POINTER(u64)]),
+        "lhaf_rpt": ([dp, dp, ip, ctypes.c_int32, dp]),
+        "lhaf_rpt_batch": ([dp, dp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32, dp]),
+        "lhaf_rpt_mixed": ([dp, dp, ip, ctypes.c_int32, dp]),
+        "lhaf_rpt_batch_dev": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
+                                ctypes.c_int32, vp, vp]),
+        "lhaf_job_create": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
+                             ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(vp)]),
+        "lhaf_job_info_get": ([vp, ctypes.POINTER(JobInfo)]),
+        "lhaf_job_reset": ([vp, vp]),
+        "lhaf_job_run": ([vp, u64, u64, vp]),
+        "lhaf_job_allreduce": ([vp, vp]),
+        "lhaf_job_finalize": ([vp, vp, ctypes.c_int32, vp]),
+        "lhaf_job_abs_sum": ([vp, dp]),
+        "lhaf_job_partials": ([vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]),
+        "lhaf_job_terms": ([vp, ctypes.POINTER(u64), ctypes.c_int32, dp]),
+        "lhaf_set_device": ([ctypes.c_int32]),
+        "lhaf_get_unique_id": ([vp]),
+        "lhaf_init_rank": ([ctypes.c_int32, ctypes.c_int32, vp, ctypes.c_int32]),
+        "lhaf_rank_info": ([ip, ip]),
+        "lhaf_set_kernel": ([ctypes.c_int32]),
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.lhaf_job_destroy.argtypes = [vp]
+    lib.lhaf_job_destroy.restype = None
+    lib.lhaf_last_error.restype = ctypes.c_char_p
+    lib.lhaf_version.restype = ctypes.c_char_p
+    lib.lhaf_shutdown.restype = None
+    return lib
+
+
+_lib = _load()
+
+# every symbol include/lhaf.h declares (checked by tests/test_capi.py)
+EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed",
+            "lhaf_rpt_batch_dev", "lhaf_job_create", "lhaf_job_info_get", "lhaf_job_reset",
+            "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_finalize", "lhaf_job_abs_sum",
+            "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
+            "lhaf_get_unique_id", "lhaf_init_rank", "lhaf_rank_info", "lhaf_set_kernel",
+            "lhaf_last_error", "lhaf_version", "lhaf_shutdown"]
+
+
+def _check(status: int):
+    if status != LHAF_OK:
+        raise LhafError(status, _lib.lhaf_last_error().decode())
+
+
+def _c128(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+
+
+def _i32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def version() -> str:
+    return _lib.lhaf_version().decode()
+
+
+def lhaf_plan(reps, mixed: bool = False) -> PlanInfo:
+    reps = _i32(reps)
+    info = PlanInfo()
+    _check(_lib.lhaf_plan(_ip(reps), reps.shape[0], int(mixed), ctypes.byref(info)))
+    return info
+
+
+def lhaf_decode(info: PlanInfo, t: int):
+    """(k digits, w, sign, weight) of term t -- integer work, bit-exact."""
+    k = np.zeros(max(1, info.H), np.int32)
+    w = np.zeros(max(1, info.H), np.int32)
+    sign = ctypes.c_int32()
+    weight = ctypes.c_uint64()
+    _check(_lib.lhaf_decode(ctypes.byref(info), int(t), _ip(k), _ip(w), ctypes.byref(sign),
+                            ctypes.byref(weight)))
+    return k[:info.H].tolist(), w[:info.H].tolist(), sign.value, weight.value
+
+
+def lhaf_rpt(A, gamma, reps) -> complex:
+    A, gamma, reps = _c128(A), _c128(gamma), _i32(reps)
+    out = np.zeros(2)
+    _check(_lib.lhaf_rpt(_dp(A), _dp(gamma), _ip(reps), reps.shape[0], _dp(out)))
+    return complex(out[0], out[1])
+
+
+def lhaf_rpt_batch(A, gamma, reps_batch, gamma_per_pattern: bool = False) -> np.ndarray:
+    A, gamma, reps = _c128(A), _c128(gamma), _i32(reps_batch)
+    batch, k = reps.shape
+    stride = gamma.shape[-1] if gamma_per_pattern else 0
+    out = np.zeros(2 * batch)
+    _check(_lib.lhaf_rpt_batch(_dp(A), _dp(gamma), stride, _ip(reps), k, batch, _dp(out)))
+    return out[0::2] + 1j * out[1::2]
+
+
+def lhaf_rpt_mixed(A2, gamma2, reps) -> complex:
+    A2, gamma2, reps = _c128(A2), _c128(gamma2), _i32(reps)
+    out = np.zeros(2)
+    _check(_lib.lhaf_rpt_mixed(_dp(A2), _dp(gamma2), _ip(reps), reps.shape[0], _dp(out)))
+    return complex(out[0], out[1])
+
+
+def lhaf_rpt_batch_dev(A_dev_ptr: int, gamma_dev_ptr: int, gamma_stride: int, reps_batch,
+                       mixed: bool, out_dev_ptr: int, stream_ptr: int = 0):
+    """Device-pointer entry (e.g. torch tensors' data_ptr() and current stream)."""
+    reps = _i32(reps_batch)
+    if reps.ndim == 1:
+        reps = reps[None, :]
+    batch, k = reps.shape
+    _check(_lib.lhaf_rpt_batch_dev(ctypes.c_void_p(A_dev_ptr), ctypes.c_void_p(gamma_dev_ptr),
+                                   gamma_stride, _ip(reps), k, batch, int(mixed),
+                                   ctypes.c_void_p(out_dev_ptr), ctypes.c_void_p(stream_ptr)))
+
+
+class Job:
+    """A planned, device-resident evaluation (lhaf_job_*).  Inputs are copied to HBM at
+    creation; ``run`` evaluates a work-unit range into the chunk-partial array."""
+
+    def __init__(self, A, gamma, reps_batch, mixed: bool = False, gamma_per_pattern: bool = False):
+        self._A, self._g, self._reps = _c128(A), _c128(gamma), _i32(reps_batch)
+        if self._reps.ndim == 1:
+            self._reps = self._reps[None, :]
+        batch, k = self._reps.shape
+        stride = self._g.shape[-1] if gamma_per_pattern else 0
+        h = ctypes.c_void_p()
+        _check(_lib.lhaf_job_create(self._A.ctypes.data,
+                                    self._g.ctypes.data, stride, _ip(self._reps), k, batch,
+                                    int(mixed), 0, ctypes.byref(h)))
+        self._h = h
+        self.info = JobInfo()
+        _check(_lib.lhaf_job_info_get(self._h, ctypes.byref(self.info)))
+
+    @property
+    def units(self) -> int:
+        return int(self.info.units)
+
+    @property
+    def terms(self) -> int:
+        return int(self.info.terms)
+
+    def reset(self, stream: int = 0):
+        _check(_lib.lhaf_job_reset(self._h, ctypes.c_void_p(stream)))
+
+    def run(self, unit_begin: int = 0, unit_end: int | None = None, stream: int = 0):
+        ue = self.units if unit_end is None else unit_end
+        _check(_lib.lhaf_job_run(self._h, unit_begin, ue, ctypes.c_void_p(stream)))
+
+    def allreduce(self, stream: int = 0):
+        _check(_lib.lhaf_job_allreduce(self._h, ctypes.c_void_p(stream)))
+
+    def finalize(self, stream: int = 0) -> np.ndarray:
+        out = np.zeros(2 * self.info.batch)
+        _check(_lib.lhaf_job_finalize(self._h, out.ctypes.data, 0, ctypes.c_void_p(stream)))
+        return out[0::2] + 1j * out[1::2]
+
+    def finalize_dev(self, out_dev_ptr: int, stream: int = 0):
+        _check(_lib.lhaf_job_finalize(self._h, ctypes.c_void_p(out_dev_ptr), 1,
+                                      ctypes.c_void_p(stream)))
+
+    def abs_sum(self) -> np.ndarray:
+        out = np.zeros(self.info.batch)
+        _check(_lib.lhaf_job_abs_sum(self._h, _dp(out)))
+        return out
+
+    def partials(self):
+        p = ctypes.c_void_p()
+        nbytes = ctypes.c_size_t()
+        _check(_lib.lhaf_job_partials(self._h, ctypes.byref(p), ctypes.byref(nbytes)))
+        return p.value, nbytes.value
+
+    def terms_g(self, ts) -> np.ndarray:
+        ts = np.ascontiguousarray(np.asarray(ts, dtype=np.uint64))
+        out = np.zeros(2 * ts.shape[0])
+        _check(_lib.lhaf_job_terms(self._h, ts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                   ts.shape[0], _dp(out)))
+        return out[0::2] + 1j * out[1::2]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lhaf_job_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def lhaf_set_device(device: int):
+    _check(_lib.lhaf_set_device(device))
+
+
+def lhaf_set_kernel(variant: int):
+    _check(_lib.lhaf_set_kernel(variant))
+
+
+def lhaf_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.lhaf_get_unique_id(buf))
+    return buf.raw
+
+
+def lhaf_init_rank(rank: int, nranks: int, uid: bytes | None, device: int = -1):
+    buf = ctypes.create_string_buffer(uid, 128) if uid is not None else None
+    _check(_lib.lhaf_init_rank(rank, nranks, buf, device))
+
+
+def lhaf_rank_info():
+    r, n = ctypes.c_int32(), ctypes.c_int32()
+    _check(_lib.lhaf_rank_info(ctypes.byref(r), ctypes.byref(n)))
+    return r.value, n.value
+
+
+def lhaf_shutdown():
+    _lib.lhaf_shutdown()

@@ -1,0 +1,43 @@
+"""Build liblhaf.so in-tree: the sm_100a kernels + the C++ host library behind include/lhaf.h.
+
+    python -m paper_2108_01622_b200.build          (or __graft_entry__.build())
+
+nvcc cross-compiles for sm_100a without a GPU.  The .so is git-ignored but travels to the GPU
+box with the gpurun snapshot.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "liblhaf.so")
+SOURCES = [os.path.join(CSRC, f) for f in ("lhaf_kernels.cu", "lhaf_host.cpp")]
+HEADERS = [os.path.join(CSRC, "lhaf_internal.h"), os.path.join(ROOT, "include", "lhaf.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+           "-Xptxas", "-v" if verbose else "-O3", "-shared", "-o", LIB, *SOURCES,
+           "-I", os.path.join(ROOT, "include"), "-ldl"]
+    subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,632 @@
+// lhaf_host.cpp -- C-ABI of include/lhaf.h: validation, greedy matching, term plans, work
+// units, device orchestration and the multi-rank NCCL exchange.  All floating-point work of
+// the method runs in the sm_100a kernels (lhaf_kernels.cu); this file does integer planning,
+// memory management and launches only.  Product code: shares nothing with oracle/.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/lhaf.h"
+#include "lhaf_internal.h"
+
+using namespace lhaf;
+
+namespace {
+
+thread_local std::string g_err;
+std::recursive_mutex g_mu;
+
+lhaf_status fail(lhaf_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) return fail(LHAF_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    return GetUniqueId && CommInitRank && AllReduce && CommDestroy && GetErrorString;
+  }
+};
+
+struct Ctx {
+  int device = -1;
+  int num_sms = 0;
+  int variant = 0;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  Nccl nccl;
+  uint64_t max_terms = (uint64_t)1 << 40;
+};
+Ctx g_ctx;
+
+lhaf_status ensure_device() {
+  if (g_ctx.device >= 0) {
+    CUDA_TRY(cudaSetDevice(g_ctx.device));
+    return LHAF_OK;
+  }
+  int dev = 0;
+  if (const char *e = getenv("LHAF_DEVICE")) dev = atoi(e);
+  int count = 0;
+  cudaError_t ce = cudaGetDeviceCount(&count);
+  if (ce != cudaSuccess || count == 0)
+    return fail(LHAF_E_CUDA, "no CUDA device available (%s); the library has no CPU path",
+                cudaGetErrorString(ce));
+  if (dev >= count) return fail(LHAF_E_CUDA, "device %d out of range (%d devices)", dev, count);
+  CUDA_TRY(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    return fail(LHAF_E_CUDA, "device %d is sm_%d%d; this build targets sm_100a only", dev,
+                prop.major, prop.minor);
+  g_ctx.device = dev;
+  g_ctx.num_sms = prop.multiProcessorCount;
+  if (const char *e = getenv("LHAF_MAX_TERMS")) g_ctx.max_terms = strtoull(e, nullptr, 10);
+  return LHAF_OK;
+}
+
+// ------------------------------------------------------------------ planning (host, integer)
+// Greedy matching of P:474-481 (reading C9).  Independent implementation from oracle/.
+struct Plan {
+  int N = 0, H = 0, d = 0, n = 0, leftover = -1;
+  uint64_t T = 1, T_eval = 0;
+  std::vector<int> p, q, eta;  // q = -1 for the phantom
+};
+
+lhaf_status make_plan(const int32_t *reps, int k, int mixed, Plan &P) {
+  P = Plan();
+  long N = 0;
+  for (int i = 0; i < k; ++i) {
+    if (reps[i] < 0) return fail(LHAF_E_ARG, "reps[%d] = %d < 0", i, reps[i]);
+    N += reps[i];
+  }
+  if (mixed) N *= 2;
+  if (N > 4 * LHAF_MAX_DEGREE) return fail(LHAF_E_TOO_LARGE, "N = %ld photons too large", N);
+  P.N = (int)N;
+  if (mixed) {
+    for (int i = 0; i < k; ++i)
+      if (reps[i] > 0) { P.p.push_back(i); P.q.push_back(i + k); P.eta.push_back(reps[i]); }
+  } else {
+    struct Item { int n, m; };
+    std::vector<Item> v;
+    for (int i = 0; i < k; ++i)
+      if (reps[i] > 0) v.push_back({reps[i], i});
+    for (;;) {
+      long tot = 0;
+      for (auto &it : v) tot += it.n;
+      if (tot <= 1) {
+        if (tot == 1) P.leftover = v[0].m;
+        break;
+      }
+      std::sort(v.begin(), v.end(), [](const Item &a, const Item &b) {
+        return a.n != b.n ? a.n > b.n : a.m < b.m;  // step 1: descending n, ties: lower mode first
+      });
+      const int n1 = v[0].n, n2 = v.size() > 1 ? v[1].n : 0;
+      if (n1 >= 2 * n2) {  // step 2: self pairs (m1, m1) x floor(n1/2)
+        P.p.push_back(v[0].m); P.q.push_back(v[0].m); P.eta.push_back(n1 / 2);
+        v[0].n -= 2 * (n1 / 2);
+      } else {             // (m1, m2) x n2
+        P.p.push_back(v[0].m); P.q.push_back(v[1].m); P.eta.push_back(n2);
+        v[0].n -= n2; v[1].n -= n2;
+      }
+      v.erase(std::remove_if(v.begin(), v.end(), [](const Item &a) { return a.n == 0; }), v.end());
+    }
+    if (P.leftover >= 0) { P.p.push_back(P.leftover); P.q.push_back(-1); P.eta.push_back(1); }
+  }
+  P.H = (int)P.eta.size();
+  if (P.H > LHAF_MAX_PAIRS) return fail(LHAF_E_TOO_LARGE, "H = %d pairs > %d", P.H, LHAF_MAX_PAIRS);
+  P.d = 2 * P.H;
+  long n = 0;
+  for (int e : P.eta) n += e;
+  P.n = (int)n;
+  P.T = 1;
+  for (int e : P.eta) {
+    const uint64_t r = (uint64_t)e + 1;
+    if (P.T > (~(uint64_t)0) / r) return fail(LHAF_E_TOO_LARGE, "term count overflows 64 bits");
+    P.T *= r;
+  }
+  P.T_eval = P.H > 0 ? P.T / 2 : 0;
+  return LHAF_OK;
+}
+
+lhaf_status check_plan_limits(const Plan &P) {
+  if (P.d > LHAF_MAX_DIM) return fail(LHAF_E_TOO_LARGE, "reduced dimension d = %d > %d", P.d, LHAF_MAX_DIM);
+  if (P.n > LHAF_MAX_DEGREE) return fail(LHAF_E_TOO_LARGE, "degree n = %d > %d", P.n, LHAF_MAX_DEGREE);
+  if (P.T_eval > g_ctx.max_terms)
+    return fail(LHAF_E_TOO_LARGE, "%llu terms > guard %llu (LHAF_MAX_TERMS)",
+                (unsigned long long)P.T_eval, (unsigned long long)g_ctx.max_terms);
+  return LHAF_OK;
+}
+
+lhaf_status check_symmetric(const double *A, int m) {
+  double amax = 0.0, dmax = 0.0;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      const double *a = A + 2 * ((size_t)i * m + j), *b = A + 2 * ((size_t)j * m + i);
+      if (!std::isfinite(a[0]) || !std::isfinite(a[1]))
+        return fail(LHAF_E_ARG, "A[%d][%d] is not finite", i, j);
+      amax = std::max(amax, std::hypot(a[0], a[1]));
+      dmax = std::max(dmax, std::hypot(a[0] - b[0], a[1] - b[1]));
+    }
+  if (dmax > 1e-12 * std::max(1.0, amax))
+    return fail(LHAF_E_NOT_SYMMETRIC, "max|A - A^T| = %.3e > 1e-12 * max(1, max|A|)", dmax);
+  return LHAF_OK;
+}
+
+uint64_t chunk_for(uint64_t T_eval) {
+  const uint64_t min_chunk = 64, max_units = 32768;
+  uint64_t c = (T_eval + max_units - 1) / max_units;
+  if (c < min_chunk) c = min_chunk;
+  if (c > T_eval) c = T_eval;
+  return c;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ job
+struct lhaf_job {
+  int batch = 0, kdim = 0, d_max = 0, n_max = 0, variant = 1;
+  bool any_loop = true;
+  uint64_t units = 0, terms = 0;
+  std::vector<PatDesc> descs;
+  // device
+  PatDesc *d_descs = nullptr;
+  int32_t *d_ipool = nullptr;
+  double *d_dpool = nullptr;
+  uint64_t *d_upool = nullptr;
+  double2 *d_cpool = nullptr;
+  double2 *d_A = nullptr, *d_gamma = nullptr;
+  bool own_inputs = true;
+  Partial *d_partials = nullptr;
+  unsigned long long *d_counter = nullptr;
+  double2 *d_out = nullptr;
+  double *d_abs = nullptr;
+  JobDev dev() const {
+    JobDev J;
+    J.descs = d_descs; J.npat = batch; J.ipool = d_ipool; J.dpool = d_dpool; J.upool = d_upool;
+    J.cpool = d_cpool; J.A = d_A; J.gamma = d_gamma; J.kdim = kdim; J.partials = d_partials;
+    J.counter = d_counter;
+    return J;
+  }
+};
+
+static void job_free(lhaf_job *j) {
+  if (!j) return;
+  cudaFree(j->d_descs); cudaFree(j->d_ipool); cudaFree(j->d_dpool); cudaFree(j->d_upool);
+  cudaFree(j->d_cpool);
+  if (j->own_inputs) { cudaFree(j->d_A); cudaFree(j->d_gamma); }
+  cudaFree(j->d_partials); cudaFree(j->d_counter); cudaFree(j->d_out); cudaFree(j->d_abs);
+  delete j;
+}
+
+template <class T>
+static cudaError_t upload(T **dst, const std::vector<T> &v) {
+  const size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+  cudaError_t e = cudaMalloc((void **)dst, bytes);
+  if (e != cudaSuccess) return e;
+  if (!v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t gamma_stride,
+                                   const int32_t *reps, int k, int batch, int mixed, bool on_device,
+                                   lhaf_job **out) {
+  if (!A || !gamma || !reps || !out) return fail(LHAF_E_ARG, "null pointer argument");
+  if (k < 0 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "k = %d out of range", k);
+  if (batch < 0) return fail(LHAF_E_ARG, "batch = %d < 0", batch);
+  const int kdim = mixed ? 2 * k : k;
+  if (gamma_stride != 0 && gamma_stride < kdim)
+    return fail(LHAF_E_ARG, "gamma_stride %lld < row length %d", (long long)gamma_stride, kdim);
+  if (!on_device) {
+    lhaf_status s = check_symmetric(A, kdim);
+    if (s != LHAF_OK) return s;
+  }
+  lhaf_status s = ensure_device();
+  if (s != LHAF_OK) return s;
+
+  lhaf_job *j = new lhaf_job();
+  j->batch = batch;
+  j->kdim = kdim;
+  j->variant = 1;
+  std::vector<int32_t> ipool;
+  std::vector<double> dpool;
+  std::vector<uint64_t> upool;
+  int64_t cpool_words = 0;
+  uint64_t unit = 0;
+  j->descs.resize(batch);
+  for (int b = 0; b < batch; ++b) {
+    Plan P;
+    s = make_plan(reps + (size_t)b * k, k, mixed, P);
+    if (s == LHAF_OK) s = check_plan_limits(P);
+    if (s != LHAF_OK) { job_free(j); return s; }
+    PatDesc &D = j->descs[b];
+    memset(&D, 0, sizeof D);
+    D.d = P.d; D.H = P.H; D.n = P.n; D.flags = 0;
+    D.T_eval = P.T_eval;
+    D.gamma_off = gamma_stride ? (int64_t)b * gamma_stride : 0;
+    D.unit_begin = unit;
+    if (P.H == 0) { D.chunk = 0; D.units = 0; continue; }
+    D.chunk = chunk_for(P.T_eval);
+    D.units = (P.T_eval + D.chunk - 1) / D.chunk;
+    unit += D.units;
+    j->terms += P.T_eval;
+    j->d_max = std::max(j->d_max, P.d);
+    j->n_max = std::max(j->n_max, P.n);
+    // index list r = (p_1..p_H, q_1..q_H)
+    D.idx_off = (int32_t)ipool.size();
+    for (int h = 0; h < P.H; ++h) ipool.push_back(P.p[h]);
+    for (int h = 0; h < P.H; ++h) ipool.push_back(P.q[h]);
+    D.eta_off = (int32_t)ipool.size();
+    for (int h = 0; h < P.H; ++h) ipool.push_back(P.eta[h]);
+    int acc = 0;
+    for (int h = 0; h < P.H; ++h) { ipool.push_back(acc); acc += P.eta[h] + 1; }
+    D.bin_off = (int32_t)dpool.size();
+    for (int h = 0; h < P.H; ++h) {
+      long double c = 1.0L;
+      for (int kk = 0; kk <= P.eta[h]; ++kk) {
+        dpool.push_back((double)c);
+        c = c * (long double)(P.eta[h] - kk) / (long double)(kk + 1);
+      }
+    }
+    D.radix_off = (int32_t)upool.size();
+    uint64_t R = 1;
+    for (int h = 0; h < P.H; ++h) { upool.push_back(R); R *= (uint64_t)(P.eta[h] + 1); }
+    D.mat_off = cpool_words;
+    cpool_words += (int64_t)P.d * P.d + 2 * P.d + 2;
+  }
+  j->units = unit;
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = upload(&j->d_descs, j->descs);
+  if (e == cudaSuccess) e = upload(&j->d_ipool, ipool);
+  if (e == cudaSuccess) e = upload(&j->d_dpool, dpool);
+  if (e == cudaSuccess) e = upload(&j->d_upool, upool);
+  if (e == cudaSuccess) e = cudaMalloc(&j->d_cpool, std::max<int64_t>(1, cpool_words) * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&j->d_partials, std::max<uint64_t>(1, j->units) * sizeof(Partial));
+  if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->units) * sizeof(Partial));
+  if (e == cudaSuccess) e = cudaMalloc(&j->d_counter, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&j->d_out, std::max(1, batch) * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&j->d_abs, std::max(1, batch) * sizeof(double));
+  const size_t gamma_rows = gamma_stride ? (size_t)batch : 1;
+  const size_t gamma_len = gamma_stride ? (size_t)batch * gamma_stride : (size_t)kdim;
+  if (on_device) {
+    j->own_inputs = false;
+    j->d_A = (double2 *)A;
+    j->d_gamma = (double2 *)gamma;
+  } else {
+    if (e == cudaSuccess) e = cudaMalloc(&j->d_A, std::max<size_t>(1, (size_t)kdim * kdim) * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc(&j->d_gamma, std::max<size_t>(1, gamma_len) * sizeof(double2));
+    if (e == cudaSuccess && kdim > 0)
+      e = cudaMemcpy(j->d_A, A, (size_t)kdim * kdim * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && gamma_len > 0)
+      e = cudaMemcpy(j->d_gamma, gamma, gamma_len * sizeof(double2), cudaMemcpyHostToDevice);
+  }
+  (void)gamma_rows;
+  if (e == cudaSuccess) e = launch_prep(j->dev(), j->d_max, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    job_free(j);
+    return fail(LHAF_E_CUDA, "job setup: %s", cudaGetErrorString(e));
+  }
+  j->variant = g_ctx.variant ? g_ctx.variant : choose_variant(j->d_max, j->n_max);
+  *out = j;
+  return LHAF_OK;
+}
+
+static void rank_units(uint64_t units, uint64_t &b, uint64_t &e) {
+  const uint64_t R = (uint64_t)g_ctx.nranks, r = (uint64_t)g_ctx.rank;
+  b = units * r / R;
+  e = units * (r + 1) / R;
+}
+
+static lhaf_status job_allreduce_impl(lhaf_job *j, cudaStream_t st) {
+  if (g_ctx.nranks <= 1 || j->units == 0) return LHAF_OK;
+  if (!g_ctx.comm) return fail(LHAF_E_STATE, "multi-rank all-reduce without a communicator");
+  const size_t count = (size_t)j->units * (sizeof(Partial) / sizeof(double));
+  ncclResult_t r = g_ctx.nccl.AllReduce(j->d_partials, j->d_partials, count, ncclDouble, ncclSum,
+                                        g_ctx.comm, st);
+  if (r != ncclSuccess) return fail(LHAF_E_NCCL, "ncclAllReduce: %s", g_ctx.nccl.GetErrorString(r));
+  return LHAF_OK;
+}
+
+static lhaf_status evaluate(lhaf_job *j, double *out_host, double *out_dev, cudaStream_t st) {
+  uint64_t b, e;
+  rank_units(j->units, b, e);
+  CUDA_TRY(cudaMemsetAsync(j->d_partials, 0, std::max<uint64_t>(1, j->units) * sizeof(Partial), st));
+  CUDA_TRY(launch_sieve(j->dev(), j->variant, j->d_max, j->n_max, b, e, g_ctx.num_sms, st));
+  lhaf_status s = job_allreduce_impl(j, st);
+  if (s != LHAF_OK) return s;
+  double2 *dst = out_dev ? (double2 *)out_dev : j->d_out;
+  CUDA_TRY(launch_finalize(j->dev(), dst, j->d_abs, st));
+  if (out_host)
+    CUDA_TRY(cudaMemcpyAsync(out_host, dst, (size_t)j->batch * sizeof(double2), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return LHAF_OK;
+}
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" {
+
+const char *lhaf_last_error(void) { return g_err.c_str(); }
+const char *lhaf_version(void) { return "lhaf-b200 0.1 (sm_100a)"; }
+
+lhaf_status lhaf_plan(const int32_t *reps, int32_t k, int32_t mixed, lhaf_plan_info *info) {
+  if (!info || (k > 0 && !reps)) return fail(LHAF_E_ARG, "null pointer argument");
+  if (k < 0 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "k = %d out of range", k);
+  Plan P;
+  lhaf_status s = make_plan(reps, k, mixed, P);
+  if (s != LHAF_OK) return s;
+  memset(info, 0, sizeof *info);
+  info->N = P.N; info->H = P.H; info->d = P.d; info->n = P.n; info->leftover = P.leftover;
+  info->T = P.T; info->T_eval = P.T_eval;
+  for (int h = 0; h < P.H; ++h) { info->p[h] = P.p[h]; info->q[h] = P.q[h]; info->eta[h] = P.eta[h]; }
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_decode(const lhaf_plan_info *info, uint64_t t, int32_t *k_out, int32_t *w_out,
+                        int32_t *sign_out, uint64_t *weight_out) {
+  if (!info || !k_out || !w_out || !sign_out || !weight_out) return fail(LHAF_E_ARG, "null pointer");
+  if (t >= info->T) return fail(LHAF_E_ARG, "t = %llu >= T", (unsigned long long)t);
+  uint64_t rem = t, weight = 1;
+  int ks = 0;
+  for (int h = 0; h < info->H; ++h) {
+    const uint64_t r = (uint64_t)info->eta[h] + 1;
+    const int kd = (int)(rem % r);
+    rem /= r;
+    k_out[h] = kd;
+    w_out[h] = info->eta[h] - 2 * kd;
+    ks += kd;
+    uint64_t c = 1;  // C(eta, kd), exact while it fits
+    for (int i = 1; i <= kd; ++i) c = c * (uint64_t)(info->eta[h] - kd + i) / (uint64_t)i;
+    weight *= c;
+  }
+  *sign_out = (ks & 1) ? -1 : 1;
+  *weight_out = weight;
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_set_device(int32_t device) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count)
+    return fail(LHAF_E_CUDA, "cannot select device %d", device);
+  g_ctx.device = -1;
+  setenv("LHAF_DEVICE", std::to_string(device).c_str(), 1);
+  return ensure_device();
+}
+
+lhaf_status lhaf_set_kernel(int32_t variant) {
+  if (variant < 0 || variant > 1) return fail(LHAF_E_ARG, "unknown kernel variant %d", variant);
+  g_ctx.variant = variant;
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_create(const double *A, const double *gamma, int64_t gamma_stride,
+                            const int32_t *reps, int32_t k, int32_t batch, int32_t mixed,
+                            int32_t A_is_device, lhaf_job **job) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  return job_create_impl(A, gamma, gamma_stride, reps, k, batch, mixed, A_is_device != 0, job);
+}
+
+lhaf_status lhaf_job_info_get(const lhaf_job *j, lhaf_job_info *info) {
+  if (!j || !info) return fail(LHAF_E_ARG, "null pointer");
+  info->batch = j->batch; info->d_max = j->d_max; info->n_max = j->n_max; info->kernel = j->variant;
+  info->units = j->units; info->terms = j->terms;
+  // model flops of the first non-empty pattern (batches here are uniform in d)
+  info->flops_per_term_model = 0.0;
+  for (const auto &D : j->descs)
+    if (D.d > 0) { info->flops_per_term_model = flops_per_term(j->variant, D.d, D.n, true); break; }
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_reset(lhaf_job *j, void *stream) {
+  if (!j) return fail(LHAF_E_ARG, "null job");
+  CUDA_TRY(cudaMemsetAsync(j->d_partials, 0, std::max<uint64_t>(1, j->units) * sizeof(Partial),
+                           (cudaStream_t)stream));
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_run(lhaf_job *j, uint64_t ub, uint64_t ue, void *stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!j) return fail(LHAF_E_ARG, "null job");
+  if (ue > j->units || ub > ue) return fail(LHAF_E_ARG, "unit range [%llu, %llu) outside [0, %llu)",
+                                            (unsigned long long)ub, (unsigned long long)ue,
+                                            (unsigned long long)j->units);
+  lhaf_status s = ensure_device();
+  if (s != LHAF_OK) return s;
+  CUDA_TRY(launch_sieve(j->dev(), j->variant, j->d_max, j->n_max, ub, ue, g_ctx.num_sms,
+                        (cudaStream_t)stream));
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_allreduce(lhaf_job *j, void *stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!j) return fail(LHAF_E_ARG, "null job");
+  return job_allreduce_impl(j, (cudaStream_t)stream);
+}
+
+lhaf_status lhaf_job_finalize(lhaf_job *j, double *out, int32_t out_is_device, void *stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!j || !out) return fail(LHAF_E_ARG, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  double2 *dst = out_is_device ? (double2 *)out : j->d_out;
+  CUDA_TRY(launch_finalize(j->dev(), dst, j->d_abs, st));
+  if (!out_is_device) {
+    CUDA_TRY(cudaMemcpyAsync(out, dst, (size_t)j->batch * sizeof(double2), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_abs_sum(lhaf_job *j, double *out) {
+  if (!j || !out) return fail(LHAF_E_ARG, "null pointer");
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(out, j->d_abs, (size_t)j->batch * sizeof(double), cudaMemcpyDeviceToHost));
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_partials(lhaf_job *j, void **dev_ptr, size_t *bytes) {
+  if (!j || !dev_ptr || !bytes) return fail(LHAF_E_ARG, "null pointer");
+  *dev_ptr = j->d_partials;
+  *bytes = (size_t)j->units * sizeof(Partial);
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_terms(lhaf_job *j, const uint64_t *t, int32_t nt, double *g_out) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!j || (nt > 0 && (!t || !g_out))) return fail(LHAF_E_ARG, "null pointer");
+  if (j->batch < 1 || j->descs[0].d == 0) return fail(LHAF_E_ARG, "pattern 0 has no terms");
+  uint64_t *dt = nullptr;
+  double2 *dg = nullptr;
+  CUDA_TRY(cudaMalloc(&dt, std::max(1, nt) * sizeof(uint64_t)));
+  CUDA_TRY(cudaMalloc(&dg, std::max(1, nt) * sizeof(double2)));
+  cudaError_t e = cudaMemcpy(dt, t, nt * sizeof(uint64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_terms(j->dev(), j->variant, j->descs[0].d, j->descs[0].n, dt, nt, dg, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(g_out, dg, nt * sizeof(double2), cudaMemcpyDeviceToHost);
+  cudaFree(dt);
+  cudaFree(dg);
+  if (e != cudaSuccess) return fail(LHAF_E_CUDA, "lhaf_job_terms: %s", cudaGetErrorString(e));
+  return LHAF_OK;
+}
+
+void lhaf_job_destroy(lhaf_job *j) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  job_free(j);
+}
+
+lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_stride,
+                           const int32_t *reps, int32_t k, int32_t batch, double *out) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!out) return fail(LHAF_E_ARG, "null output");
+  lhaf_job *j = nullptr;
+  lhaf_status s = job_create_impl(A, gamma, gamma_stride, reps, k, batch, 0, false, &j);
+  if (s != LHAF_OK) return s;
+  std::vector<double> tmp((size_t)std::max(1, batch) * 2);
+  s = evaluate(j, tmp.data(), nullptr, 0);
+  job_free(j);
+  if (s == LHAF_OK) memcpy(out, tmp.data(), (size_t)batch * 2 * sizeof(double));
+  return s;
+}
+
+lhaf_status lhaf_rpt(const double *A, const double *gamma, const int32_t *reps, int32_t k,
+                     double out[2]) {
+  return lhaf_rpt_batch(A, gamma, 0, reps, k, 1, out);
+}
+
+lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t *reps, int32_t k,
+                           double out[2]) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!out) return fail(LHAF_E_ARG, "null output");
+  lhaf_job *j = nullptr;
+  lhaf_status s = job_create_impl(A2, gamma2, 0, reps, k, 1, 1, false, &j);
+  if (s != LHAF_OK) return s;
+  double tmp[2];
+  s = evaluate(j, tmp, nullptr, 0);
+  job_free(j);
+  if (s == LHAF_OK) { out[0] = tmp[0]; out[1] = tmp[1]; }
+  return s;
+}
+
+lhaf_status lhaf_rpt_batch_dev(const double *A_dev, const double *gamma_dev, int64_t gamma_stride,
+                               const int32_t *reps, int32_t k, int32_t batch, int32_t mixed,
+                               double *out_dev, void *stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!out_dev) return fail(LHAF_E_ARG, "null output");
+  lhaf_job *j = nullptr;
+  lhaf_status s = job_create_impl(A_dev, gamma_dev, gamma_stride, reps, k, batch, mixed, true, &j);
+  if (s != LHAF_OK) return s;
+  s = evaluate(j, nullptr, out_dev, (cudaStream_t)stream);
+  job_free(j);
+  return s;
+}
+
+lhaf_status lhaf_get_unique_id(void *id128) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!id128) return fail(LHAF_E_ARG, "null pointer");
+  if (!g_ctx.nccl.load()) return fail(LHAF_E_NCCL, "cannot dlopen libnccl.so.2");
+  ncclUniqueId id;
+  ncclResult_t r = g_ctx.nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(LHAF_E_NCCL, "ncclGetUniqueId: %s", g_ctx.nccl.GetErrorString(r));
+  memcpy(id128, &id, sizeof id);
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_init_rank(int32_t rank, int32_t nranks, const void *id128, int32_t device) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LHAF_E_ARG, "bad rank %d of %d", rank, nranks);
+  if (device >= 0) {
+    lhaf_status s = lhaf_set_device(device);
+    if (s != LHAF_OK) return s;
+  } else {
+    lhaf_status s = ensure_device();
+    if (s != LHAF_OK) return s;
+  }
+  if (g_ctx.comm) { g_ctx.nccl.CommDestroy(g_ctx.comm); g_ctx.comm = nullptr; }
+  g_ctx.rank = rank;
+  g_ctx.nranks = nranks;
+  if (nranks == 1) return LHAF_OK;
+  if (!id128) return fail(LHAF_E_ARG, "null unique id");
+  if (!g_ctx.nccl.load()) return fail(LHAF_E_NCCL, "cannot dlopen libnccl.so.2");
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof id);
+  ncclResult_t r = g_ctx.nccl.CommInitRank(&g_ctx.comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    g_ctx.nranks = 1; g_ctx.rank = 0;
+    return fail(LHAF_E_NCCL, "ncclCommInitRank: %s", g_ctx.nccl.GetErrorString(r));
+  }
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_rank_info(int32_t *rank, int32_t *nranks) {
+  if (!rank || !nranks) return fail(LHAF_E_ARG, "null pointer");
+  *rank = g_ctx.rank;
+  *nranks = g_ctx.nranks;
+  return LHAF_OK;
+}
+
+void lhaf_shutdown(void) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (g_ctx.comm) { g_ctx.nccl.CommDestroy(g_ctx.comm); g_ctx.comm = nullptr; }
+  g_ctx.rank = 0;
+  g_ctx.nranks = 1;
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// lhaf_internal.h -- structures shared by the host planner (lhaf_host.cpp) and the sm_100a
+// kernels (lhaf_kernels.cu).  Product code only: the oracle (oracle/) never includes this.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lhaf {
+
+// One pattern of a job.  All offsets index the job's device pools.
+struct PatDesc {
+  int32_t d;           // reduced dimension 2H (0 when N = 0)
+  int32_t H;           // pairs incl. phantom
+  int32_t n;           // lambda degree = sum eta
+  int32_t flags;       // bit 0: loop vector nonzero (loop terms present)
+  uint64_t T_eval;     // evaluated terms floor(T/2)
+  uint64_t chunk;      // terms per work unit
+  uint64_t unit_begin; // first global work unit of this pattern
+  uint64_t units;      // number of work units
+  int32_t idx_off;     // ipool: r[d] (mode index of reduced row a; -1 = phantom)
+  int32_t eta_off;     // ipool: eta[H]
+  int32_t bin_off;     // dpool: for pair h, C(eta_h, k) k = 0..eta_h, concatenated
+  int32_t radix_off;   // upool: R_h = prod_{h' < h} (eta_h' + 1)
+  int64_t mat_off;     // cpool (double2): Ct[d*d] | uh[d] | v[d] | beta[1]
+  int64_t gamma_off;   // offset (in complex entries) of this pattern's gamma row
+};
+
+constexpr uint32_t FLAG_LOOP = 1u;
+
+// Chunk partial: double-double complex sum of the unit's terms + sum |term|.
+struct Partial {
+  double re_hi, re_lo, im_hi, im_lo;
+  double abs_hi, abs_lo;
+  double pad0, pad1;
+};
+
+struct JobDev {
+  const PatDesc *descs;
+  int32_t npat;
+  const int32_t *ipool;
+  const double *dpool;
+  const uint64_t *upool;
+  double2 *cpool;
+  const double2 *A;      // k x k (or 2k x 2k) matrix
+  const double2 *gamma;  // gamma rows
+  int32_t kdim;          // row length of A (k, or 2k for mixed)
+  Partial *partials;
+  unsigned long long *counter;
+};
+
+// Launchers (lhaf_kernels.cu).  Return cudaError_t of the launch.
+cudaError_t launch_prep(const JobDev &job, int d_max, cudaStream_t s);
+cudaError_t launch_sieve(const JobDev &job, int variant, int d_max, int n_max,
+                         uint64_t unit_begin, uint64_t unit_end, int num_sms, cudaStream_t s);
+cudaError_t launch_finalize(const JobDev &job, double2 *out, double *abs_out, cudaStream_t s);
+cudaError_t launch_terms(const JobDev &job, int variant, int d_max, int n_max, const uint64_t *t,
+                         int nt, double2 *g_out, cudaStream_t s);
+// Algorithmic FP64 flops per term of a variant at (d, n) -- DESIGN.md "Roofline".
+double flops_per_term(int variant, int d, int n, bool loops);
+int choose_variant(int d_max, int n_max);
+
+}  // namespace lhaf
