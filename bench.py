@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""bench.py -- sieve terms/s and seconds per loop hafnian on B200 (BASELINE.json metric).
+
+Workload (default `--workload cfg4`): BASELINE.json config 4, the n = 60 loop hafnian
+(Haar m = 100, tanh r = 0.9, gamma sigma = 0.1, 60 photons in 60 distinct modes: d = 60,
+2^29 evaluated sieve terms).  One "step" is one pass of the whole hot path (S8(a) a4-a12:
+decode, scale, Hessenberg, La Budde, loop terms, series, compensated accumulate, all-reduce,
+finalize) over one fixed slice of the lhaf's work units; the lhaf is cut into `--slices`
+(default 32) contiguous slices, so K = 32 timed steps evaluate the whole loop hafnian once
+and `s_per_lhaf` is then measured, not extrapolated.  Other workloads: cfg2 (the 4096-pattern
+batch, one step = the whole batch), cfg3 (n = 40 collision-heavy lhaf), cfg5 (mixed state).
+
+Timing: W untimed warm-up steps; then barrier + cuda synchronize, CUDA events on the launch
+stream around exactly K steps, synchronize + barrier; max over ranks.  Between steps a 256 MiB
+buffer is written (L2 flush, inside the timed region; ~40 us per step).  nvidia-smi samples
+SM clocks and throttle reasons during the timed region.  The e2e number times the public
+C-ABI call (lhaf_rpt with host buffers: H2D copies of A/gamma/plan, D2H of the result) for
+one whole loop hafnian.  The roofline kernel time is measured with CUDA events around the
+sieve launches on the same stream.
+
+Multi-GPU: launched with torchrun; one process per GPU; NCCL communicator of the library
+bootstrapped through torch.distributed; each step's slice is split across ranks (strong
+scaling of a single lhaf, one ncclAllReduce of chunk partials per step).
+
+`--impl reference` times the CPU oracle (oracle/, long double, OpenMP) on a bounded sample of
+the same workload's terms (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gbs_inputs as G  # noqa: E402
+
+WORKLOADS = {
+    "cfg4": dict(cfg=4, slices=32, desc="BASELINE config 4: single n=60 loop hafnian, m=100 Haar, tanh r=0.9, gamma sigma=0.1, 60 distinct modes, 2^29 evaluated terms at d=60"),
+    "cfg2": dict(cfg=2, slices=1, desc="BASELINE config 2: batch of 4096 loop hafnians, N=24 distinct modes of m=50, 2^11 evaluated terms each at d=24"),
+    "cfg3": dict(cfg=3, slices=1, desc="BASELINE config 3: n=40 collision-heavy loop hafnian, 16 modes of m=100, gamma=0"),
+    "cfg5": dict(cfg=5, slices=64, desc="BASELINE config 5: mixed-state lhaf, 36 photons over 24 modes, eta=0.3, 2k=200, natural pairing, d=48"),
+}
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
+
+
+def fp64_peak():
+    """Measured FP64 DFMA peak (tools/ubench, committed under profiles/), else spec-derived."""
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            j = json.load(f)
+        return float(j["fp64_tflops_sustained"]), "measured DFMA microbenchmark (profiles/fp64_peak.json)"
+    except Exception:
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "spec-derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_workload(name):
+    w = WORKLOADS[name]
+    cfg = G.config(w["cfg"])
+    reps = cfg.get("reps_batch", cfg.get("reps"))
+    return w, cfg, reps
+
+
+def run_reference(args, rank):
+    """CPU oracle arm: the oracle as it stands, on a bounded sample of the workload's terms."""
+    if rank != 0:
+        return
+    import oracle
+    w, cfg, reps = load_workload(args.workload)
+    r0 = reps[0] if reps.ndim == 2 else reps
+    nthreads = oracle.num_threads()
+    per_step = args.ref_terms
+    t_total = 0.0
+    terms = 0
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, c = oracle.fds_range(cfg["A"], cfg["gamma"], r0, s * per_step, (s + 1) * per_step,
+                                mixed=cfg["mixed"])
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            t_total += dt
+            terms += c
+    val = terms / t_total
+    line = {
+        "impl": "reference", "metric": "sieve terms/s", "value": val, "unit": "terms/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f80 (x87 long double)", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": w["desc"]},
+        "cpu_baseline": {"value": val, "unit": "terms/s", "cores": nthreads, "kind": "oracle",
+                         "sample": f"{per_step} consecutive sieve terms per step of {args.workload} via oracle.fds_range (explicit long-double powers)"},
+        "e2e": {"value": val, "unit": "terms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(cfg, reps, seconds_target=15.0):
+    import oracle
+    r0 = reps[0] if reps.ndim == 2 else reps
+    nthreads = oracle.num_threads()
+    n = max(nthreads, 16)
+    t0 = time.perf_counter()
+    oracle.fds_range(cfg["A"], cfg["gamma"], r0, 0, n, mixed=cfg["mixed"])
+    dt = time.perf_counter() - t0
+    n2 = int(max(n, min(200000, n * seconds_target / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    _, c = oracle.fds_range(cfg["A"], cfg["gamma"], r0, n, n + n2, mixed=cfg["mixed"])
+    dt = time.perf_counter() - t0
+    return {"value": c / dt, "unit": "terms/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"{c} consecutive sieve terms of the workload's pattern 0 via oracle.fds_range, {dt:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--slices", type=int, default=None)
+    ap.add_argument("--kernel", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-terms", type=int, default=256)
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    slices = args.slices or w["slices"]
+    if args.steps is None:
+        args.steps = slices if slices > 1 else 5
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2108_01622_b200 as L
+    if args.kernel:
+        L.lhaf_set_kernel(args.kernel)
+    if world > 1:
+        uid = [L.lhaf_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        L.lhaf_init_rank(rank, world, uid[0], local)
+    else:
+        L.lhaf_set_device(local)
+
+    w, cfg, reps = load_workload(args.workload)
+    job = L.Job(cfg["A"], cfg["gamma"], reps, mixed=cfg["mixed"])
+    U = job.units
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    out_dev = torch.zeros(2 * job.info.batch, dtype=torch.float64, device="cuda")
+
+    def slice_units(s):
+        s %= slices
+        b, e = U * s // slices, U * (s + 1) // slices
+        return b + (e - b) * rank // world, b + (e - b) * (rank + 1) // world
+
+    kernel_ev = []
+
+    def step(s, record=False):
+        flush.fill_(float(s))
+        ub, ue = slice_units(s)
+        if record:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        job.run(ub, ue, sp)
+        if record:
+            b.record(stream)
+            kernel_ev.append((a, b, ue - ub))
+        job.allreduce(sp)
+        job.finalize_dev(out_dev.data_ptr(), sp)
+
+    # warm-up
+    job.reset(sp)
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    job.reset(sp)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for s in range(args.steps):
+            step(s, record=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    kernel_ms = sum(a.elapsed_time(b) for a, b, _ in kernel_ev)
+    units_timed = sum(n for _, _, n in kernel_ev)
+    terms_per_unit = job.terms / U
+    my_terms = units_timed * terms_per_unit
+    if world > 1:
+        t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kernel_ms_max = float(t[0]), float(t[1])
+        tt = torch.tensor([my_terms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt)
+        total_terms = float(tt[0])
+    else:
+        kernel_ms_max = kernel_ms
+        total_terms = my_terms
+    value = total_terms / (ms * 1e-3)
+    result = out_dev.cpu().numpy()
+    full_cover = args.steps >= slices
+    s_per_lhaf = (ms * 1e-3 * slices / args.steps) if job.info.batch == 1 else None
+
+    # roofline: algorithmic FP64 flops per launch / launch duration, vs measured DFMA peak
+    flops_term = job.info.flops_per_term_model
+    peak, peak_src = fp64_peak()
+    achieved = my_terms * flops_term / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else None
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "peak_source": peak_src, "flops_per_term": flops_term,
+                "kernel_share_of_step": kernel_ms / ms if ms > 0 else None}
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            tj = json.load(open(traffic_file))
+            roofline["traffic"] = tj.get(args.workload)
+        except Exception:
+            pass
+
+    # e2e: the public C-ABI call with host buffers (whole loop hafnian / whole batch)
+    e2e = None
+    if not args.no_e2e:
+        A = np.ascontiguousarray(cfg["A"])
+        gm = np.ascontiguousarray(cfg["gamma"])
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if cfg["mixed"]:
+            v = L.lhaf_rpt_mixed(A, gm, reps)
+        elif reps.ndim == 2:
+            v = L.lhaf_rpt_batch(A, gm, reps)
+        else:
+            v = L.lhaf_rpt(A, gm, reps)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t[0])
+        h2d = A.nbytes + gm.nbytes + int(job.info.h2d_plan_bytes)
+        d2h = 16 * job.info.batch
+        e2e = {"value": job.terms / dt, "unit": "terms/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "s_per_call": dt,
+               "call": "lhaf_rpt_mixed" if cfg["mixed"] else ("lhaf_rpt_batch" if reps.ndim == 2 else "lhaf_rpt"),
+               "result_first": [complex(np.atleast_1d(v)[0]).real, complex(np.atleast_1d(v)[0]).imag]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline_sample(cfg, reps)
+        except Exception as ex:  # the oracle is test infrastructure; never fatal for the bench
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": "sieve terms/s", "value": value, "unit": "terms/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "desc": w["desc"], "slices": slices,
+                       "units": U, "terms_per_lhaf": job.terms, "d": job.info.d_max,
+                       "n": job.info.n_max, "kernel_variant": job.info.kernel,
+                       "l2": "256 MiB buffer written before every step (inside the timed region)",
+                       "parallelism": f"term-range shards x{world}"},
+            "s_per_lhaf": s_per_lhaf if full_cover else None,
+            "s_per_lhaf_extrapolated": None if full_cover else s_per_lhaf,
+            "result": [float(result[0]), float(result[1])] if full_cover and job.info.batch == 1 else None,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 2 * len(kernel_ev),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    job.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -132,6 +132,7 @@ typedef struct {
   uint64_t units;        /* total work units */
   uint64_t terms;        /* total evaluated terms (sum of T_eval) */
   double flops_per_term_model; /* algorithmic FP64 flops per term of the selected kernel */
+  uint64_t h2d_plan_bytes;     /* bytes of plan tables copied host->device at creation */
 } lhaf_job_info;
 
 lhaf_status lhaf_job_create(const double *A, const double *gamma, int64_t gamma_stride,
@@ -163,6 +164,11 @@ lhaf_status lhaf_set_device(int32_t device);
 lhaf_status lhaf_get_unique_id(void *id128);
 lhaf_status lhaf_init_rank(int32_t rank, int32_t nranks, const void *id128, int32_t device);
 lhaf_status lhaf_rank_info(int32_t *rank, int32_t *nranks);
+/* The contiguous block of work units [*begin, *end) that rank `rank` of `nranks` evaluates
+ * out of `units` (S8(e): units are rank-independent, so results are bit-identical for any
+ * nranks).  Host-only integer arithmetic. */
+lhaf_status lhaf_shard_units(uint64_t units, int32_t rank, int32_t nranks, uint64_t *begin,
+                             uint64_t *end);
 
 /* Kernel override for experiments: 0 = automatic, else a variant id. */
 lhaf_status lhaf_set_kernel(int32_t variant);

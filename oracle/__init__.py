@@ -224,3 +224,29 @@ def decode(t: int, eta):
     for e, kk in zip(eta, ks):
         weight *= comb(e, kk)
     return ks, w, sign, weight
+
+
+def fds_range(A, gamma, reps, t0: int, t1: int, mixed: bool = False):
+    """Timing helper for bench.py's CPU baseline: sum of sieve terms [t0, t1) (no prefactor).
+    Returns (partial sum, number of terms evaluated)."""
+    lib = _load()
+    if not hasattr(lib, "_range_ready"):
+        dp = ctypes.POINTER(ctypes.c_double)
+        ip = ctypes.POINTER(ctypes.c_int32)
+        lib.orc_fds_range.argtypes = [dp, dp, ip, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                      ctypes.c_uint64, dp]
+        lib.orc_fds_range.restype = ctypes.c_uint64
+        lib.orc_num_threads.restype = ctypes.c_int
+        lib._range_ready = True
+    A = _cplx(A)
+    gamma = _cplx(gamma)
+    reps = np.ascontiguousarray(np.asarray(reps, dtype=np.int32))
+    out = np.zeros(2)
+    cnt = lib.orc_fds_range(_dptr(A), _dptr(gamma), _iptr(reps), reps.shape[0], int(mixed),
+                            t0, t1, _dptr(out))
+    return complex(out[0], out[1]), int(cnt)
+
+
+def num_threads() -> int:
+    fds_range(np.zeros((1, 1)), np.zeros(1), [0], 0, 0)
+    return int(_load().orc_num_threads())

@@ -31,6 +31,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <omp.h>
 
 typedef long double _Complex cld;
 
@@ -417,4 +418,70 @@ uint64_t orc_lhaf_fds(const double *A, const double *gamma, const int32_t *reps,
   *out_abs = (double)(sabs * scale);
   free(C); free(v);
   return T;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Timing entry for the CPU baseline: sum of the sieve terms t in [t0, t1) of the same sum as
+ * orc_lhaf_fds (each term by explicit powers), without the 2^{-n} prefactor.  Used only by
+ * bench.py's cpu_baseline / --impl reference legs; same arithmetic as orc_lhaf_fds. */
+uint64_t orc_fds_range(const double *A, const double *gamma, const int32_t *reps, int32_t k,
+                       int32_t mixed, uint64_t t0, uint64_t t1, double *out) {
+  int32_t p[256], q[256], eta[256], leftover = -1, H = 0;
+  if (!mixed) {
+    H = orc_matched_reps(reps, k, p, q, eta, 255, &leftover);
+    if (H < 0) return 0;
+  } else {
+    for (int i = 0; i < k; ++i)
+      if (reps[i] > 0) { p[H] = i; q[H] = i + k; eta[H] = reps[i]; ++H; }
+  }
+  int kk = mixed ? 2 * k : k;
+  int Hf = H + (leftover >= 0 ? 1 : 0);
+  int r[512];
+  for (int h = 0; h < H; ++h) { r[h] = p[h]; r[h + Hf] = q[h]; }
+  if (leftover >= 0) { r[H] = leftover; r[H + Hf] = -1; eta[H] = 1; }
+  int n = 0;
+  for (int h = 0; h < Hf; ++h) n += eta[h];
+  if (Hf == 0) { out[0] = 1.0; out[1] = 0.0; return 0; }
+  int dim = 2 * Hf;
+  cld *C = (cld *)malloc(sizeof(cld) * dim * dim);
+  cld *v = (cld *)malloc(sizeof(cld) * dim);
+  reduced(A, gamma, kk, Hf, r, C, v);
+  uint64_t T = 1;
+  for (int h = 0; h < Hf; ++h) T *= (uint64_t)(eta[h] + 1);
+  if (t1 > T) t1 = T;
+  long double sre = 0.0L, sim = 0.0L;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : sre, sim)
+  for (uint64_t t = t0; t < t1; ++t) {
+    int32_t w[256];
+    uint64_t rem = t;
+    int ksum = 0;
+    long double weight = 1.0L;
+    for (int h = 0; h < Hf; ++h) {
+      int kh = (int)(rem % (uint64_t)(eta[h] + 1));
+      rem /= (uint64_t)(eta[h] + 1);
+      ksum += kh;
+      long double b = 1.0L;
+      for (int i = 1; i <= kh; ++i) b = b * (long double)(eta[h] - kh + i) / (long double)i;
+      weight *= b;
+      w[h] = eta[h] - 2 * kh;
+    }
+    cld g = fds_term_ld(Hf, C, v, w, n);
+    long double sgn = (ksum & 1) ? -1.0L : 1.0L;
+    sre += sgn * weight * creall(g);
+    sim += sgn * weight * cimagl(g);
+  }
+  out[0] = (double)sre;
+  out[1] = (double)sim;
+  free(C); free(v);
+  return t1 > t0 ? t1 - t0 : 0;
+}
+
+int orc_num_threads(void) {
+  int n = 1;
+#pragma omp parallel
+  {
+#pragma omp single
+    n = omp_get_num_threads();
+  }
+  return n;
 }

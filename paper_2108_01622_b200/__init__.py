@@ -48,7 +48,7 @@ class PlanInfo(ctypes.Structure):
 class JobInfo(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("d_max", ctypes.c_int32), ("n_max", ctypes.c_int32),
                 ("kernel", ctypes.c_int32), ("units", ctypes.c_uint64), ("terms", ctypes.c_uint64),
-                ("flops_per_term_model", ctypes.c_double)]
+                ("flops_per_term_model", ctypes.c_double), ("h2d_plan_bytes", ctypes.c_uint64)]
 
 
 def _load() -> ctypes.CDLL:
@@ -83,6 +83,8 @@ def _load() -> ctypes.CDLL:
         "lhaf_init_rank": ([ctypes.c_int32, ctypes.c_int32, vp, ctypes.c_int32]),
         "lhaf_rank_info": ([ip, ip]),
         "lhaf_set_kernel": ([ctypes.c_int32]),
+        "lhaf_shard_units": ([u64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(u64),
+                              ctypes.POINTER(u64)]),
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -96,7 +98,28 @@ def _load() -> ctypes.CDLL:
     return lib
 
 
-_lib = _load()
+class _Missing:
+    """Stands in for liblhaf.so when it could not be loaded (e.g. while `build` itself is being
+    imported to rebuild it): every use raises the load error -- there is no CPU fallback."""
+
+    def __init__(self, err: Exception):
+        self._err = err
+
+    def __getattr__(self, name):
+        raise ImportError(f"liblhaf.so unavailable: {self._err}")
+
+
+try:
+    _lib = _load()
+except (OSError, AttributeError, ImportError) as _e:  # stale or missing .so
+    _lib = _Missing(_e)
+
+
+def reload_library():
+    """Re-load liblhaf.so after a rebuild (used by build())."""
+    global _lib
+    _lib = _load()
+    return _lib
 
 # every symbol include/lhaf.h declares (checked by tests/test_capi.py)
 EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed",
@@ -104,7 +127,7 @@ EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_
             "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_finalize", "lhaf_job_abs_sum",
             "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
             "lhaf_get_unique_id", "lhaf_init_rank", "lhaf_rank_info", "lhaf_set_kernel",
-            "lhaf_last_error", "lhaf_version", "lhaf_shutdown"]
+            "lhaf_shard_units", "lhaf_last_error", "lhaf_version", "lhaf_shutdown"]
 
 
 def _check(status: int):
@@ -283,6 +306,12 @@ def lhaf_rank_info():
     r, n = ctypes.c_int32(), ctypes.c_int32()
     _check(_lib.lhaf_rank_info(ctypes.byref(r), ctypes.byref(n)))
     return r.value, n.value
+
+
+def lhaf_shard_units(units: int, rank: int, nranks: int):
+    b, e = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(_lib.lhaf_shard_units(units, rank, nranks, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
 
 
 def lhaf_shutdown():

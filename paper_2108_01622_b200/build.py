@@ -35,6 +35,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-v" if verbose else "-O3", "-shared", "-o", LIB, *SOURCES,
            "-I", os.path.join(ROOT, "include"), "-ldl"]
     subprocess.check_call(cmd)
+    pkg = sys.modules.get("paper_2108_01622_b200")
+    if pkg is not None and hasattr(pkg, "reload_library"):
+        try:  # a stale copy already mapped in this process cannot be replaced; new processes load the new one
+            pkg.reload_library()
+        except (OSError, AttributeError):
+            pass
     return LIB
 
 

@@ -206,7 +206,7 @@ uint64_t chunk_for(uint64_t T_eval) {
 struct lhaf_job {
   int batch = 0, kdim = 0, d_max = 0, n_max = 0, variant = 1;
   bool any_loop = true;
-  uint64_t units = 0, terms = 0;
+  uint64_t units = 0, terms = 0, plan_bytes = 0;
   std::vector<PatDesc> descs;
   // device
   PatDesc *d_descs = nullptr;
@@ -314,6 +314,8 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     cpool_words += (int64_t)P.d * P.d + 2 * P.d + 2;
   }
   j->units = unit;
+  j->plan_bytes = j->descs.size() * sizeof(PatDesc) + ipool.size() * 4 + dpool.size() * 8 +
+                  upool.size() * 8;
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&j->d_descs, j->descs);
   if (e == cudaSuccess) e = upload(&j->d_ipool, ipool);
@@ -351,10 +353,14 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   return LHAF_OK;
 }
 
+static void shard(uint64_t units, uint64_t r, uint64_t R, uint64_t &b, uint64_t &e) {
+  // units * r / R without 64-bit overflow (units < 2^40 guard, R <= 2^16)
+  b = (uint64_t)(((unsigned __int128)units * r) / R);
+  e = (uint64_t)(((unsigned __int128)units * (r + 1)) / R);
+}
+
 static void rank_units(uint64_t units, uint64_t &b, uint64_t &e) {
-  const uint64_t R = (uint64_t)g_ctx.nranks, r = (uint64_t)g_ctx.rank;
-  b = units * r / R;
-  e = units * (r + 1) / R;
+  shard(units, (uint64_t)g_ctx.rank, (uint64_t)g_ctx.nranks, b, e);
 }
 
 static lhaf_status job_allreduce_impl(lhaf_job *j, cudaStream_t st) {
@@ -449,7 +455,7 @@ lhaf_status lhaf_job_create(const double *A, const double *gamma, int64_t gamma_
 lhaf_status lhaf_job_info_get(const lhaf_job *j, lhaf_job_info *info) {
   if (!j || !info) return fail(LHAF_E_ARG, "null pointer");
   info->batch = j->batch; info->d_max = j->d_max; info->n_max = j->n_max; info->kernel = j->variant;
-  info->units = j->units; info->terms = j->terms;
+  info->units = j->units; info->terms = j->terms; info->h2d_plan_bytes = j->plan_bytes;
   // model flops of the first non-empty pattern (batches here are uniform in d)
   info->flops_per_term_model = 0.0;
   for (const auto &D : j->descs)
@@ -619,6 +625,14 @@ lhaf_status lhaf_rank_info(int32_t *rank, int32_t *nranks) {
   if (!rank || !nranks) return fail(LHAF_E_ARG, "null pointer");
   *rank = g_ctx.rank;
   *nranks = g_ctx.nranks;
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_shard_units(uint64_t units, int32_t rank, int32_t nranks, uint64_t *begin,
+                             uint64_t *end) {
+  if (!begin || !end) return fail(LHAF_E_ARG, "null pointer");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LHAF_E_ARG, "bad rank %d of %d", rank, nranks);
+  shard(units, (uint64_t)rank, (uint64_t)nranks, *begin, *end);
   return LHAF_OK;
 }
 

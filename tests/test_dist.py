@@ -1,0 +1,98 @@
+"""N > 1 host logic on CPU (gloo, world_size 2): the library's work-unit sharding is a
+partition into contiguous blocks; an all-reduce (sum) of disjoint-support chunk-partial arrays
+reproduces the single-process array exactly (x + 0 = x), so the ordered double-double finalize
+is bit-identical for any rank count.  The GPU kernels are not involved here."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def partial_value(u):
+    """A deterministic, 'ugly' double-double partial per unit (stands in for a chunk sum)."""
+    rng = np.random.Generator(np.random.PCG64(1000 + u))
+    hi = rng.standard_normal(2) * 10.0 ** rng.integers(-8, 8, 2)
+    lo = hi * 2.0 ** -60 * rng.standard_normal(2)
+    return np.array([hi[0], lo[0], hi[1], lo[1], abs(hi[0]), 0.0, 0.0, 0.0])
+
+
+def two_sum(a, b):
+    s = a + b
+    bb = s - a
+    return s, (a - (s - bb)) + (b - bb)
+
+
+def dd_finalize(P):
+    """Python mirror of the finalize order: dd-sum units in ascending order."""
+    out = []
+    for c in (0, 2):
+        hi = lo = 0.0
+        for u in range(P.shape[0]):
+            s, e = two_sum(hi, P[u, c])
+            e += lo + P[u, c + 1]
+            hi = s + e
+            lo = e - (hi - s)
+        out.append(hi + lo)
+    return out
+
+
+def _worker(rank, world, port, units, q):
+    import paper_2108_01622_b200 as L
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, e = L.lhaf_shard_units(units, rank, world)
+    P = np.zeros((units, 8))
+    for u in range(b, e):
+        P[u] = partial_value(u)
+    t = torch.from_numpy(P)
+    dist.all_reduce(t)
+    q.put((rank, b, e, t.numpy().tobytes()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("units,world", [(37, 2), (8192, 2), (5, 2)])
+def test_sharded_partials_allreduce_exact(lib, units, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, units, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    # contiguous partition of [0, units)
+    assert res[0][1] == 0 and res[-1][2] == units
+    for a, b in zip(res, res[1:]):
+        assert a[2] == b[1]
+    full = np.stack([partial_value(u) for u in range(units)])
+    for _, _, _, buf in res:
+        got = np.frombuffer(buf, dtype=np.float64).reshape(units, 8)
+        assert np.array_equal(got, full)                 # exact: disjoint support
+        assert dd_finalize(got) == dd_finalize(full)    # hence bit-identical finalize
+
+
+def test_shard_units_partition_many_ranks(lib):
+    for units in (1, 7, 32768, 2 ** 35 + 3):
+        for R in (1, 2, 3, 4, 8, 16):
+            prev = 0
+            for r in range(R):
+                b, e = lib.lhaf_shard_units(units, r, R)
+                assert b == prev and e >= b
+                prev = e
+            assert prev == units
