@@ -193,7 +193,15 @@ lhaf_status check_symmetric(const double *A, int m) {
 }
 
 uint64_t chunk_for(uint64_t T_eval) {
-  const uint64_t min_chunk = 64, max_units = 32768;
+  // Terms per work unit: T_eval split into at most 32768 units of >= 64 terms (independent
+  // of the number of ranks, so results are bit-identical for any rank count).  LHAF_MAX_UNITS
+  // overrides the unit cap (profiling runs use small units to fill the GPU with few terms).
+  static const uint64_t max_units = [] {
+    const char *e = getenv("LHAF_MAX_UNITS");
+    const uint64_t v = e ? strtoull(e, nullptr, 10) : 0;
+    return v ? v : (uint64_t)32768;
+  }();
+  const uint64_t min_chunk = 64;
   uint64_t c = (T_eval + max_units - 1) / max_units;
   if (c < min_chunk) c = min_chunk;
   if (c > T_eval) c = T_eval;
@@ -205,7 +213,8 @@ uint64_t chunk_for(uint64_t T_eval) {
 // ------------------------------------------------------------------ job
 struct lhaf_job {
   int batch = 0, kdim = 0, d_max = 0, n_max = 0, variant = 1;
-  bool any_loop = true;
+  int e_max = 0, ntl_max = 0;   // v2: bordered dimension and leading coefficients
+  bool any_loop = false;
   uint64_t units = 0, terms = 0, plan_bytes = 0;
   std::vector<PatDesc> descs;
   // device
@@ -263,6 +272,17 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   lhaf_status s = ensure_device();
   if (s != LHAF_OK) return s;
 
+  // host view of gamma (loop flags are planned on the host)
+  const size_t gamma_len = gamma_stride ? (size_t)batch * gamma_stride : (size_t)kdim;
+  std::vector<double> gcopy;
+  const double *ghost = gamma;
+  if (on_device) {
+    gcopy.resize(2 * std::max<size_t>(1, gamma_len));
+    if (gamma_len > 0 && cudaMemcpy(gcopy.data(), gamma, gamma_len * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(LHAF_E_CUDA, "reading gamma from the device failed");
+    ghost = gcopy.data();
+  }
+
   lhaf_job *j = new lhaf_job();
   j->batch = batch;
   j->kdim = kdim;
@@ -281,6 +301,22 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     PatDesc &D = j->descs[b];
     memset(&D, 0, sizeof D);
     D.d = P.d; D.H = P.H; D.n = P.n; D.flags = 0;
+    {
+      bool loops = P.leftover >= 0;  // the phantom carries loop weight 1 (reading C7)
+      const double *gb = ghost + 2 * (size_t)(gamma_stride ? (size_t)b * gamma_stride : 0);
+      for (int h = 0; h < P.H && !loops; ++h)
+        for (int side = 0; side < 2 && !loops; ++side) {
+          const int m = side ? P.q[h] : P.p[h];
+          if (m >= 0 && (gb[2 * m] != 0.0 || gb[2 * m + 1] != 0.0)) loops = true;
+        }
+      if (loops) D.flags |= FLAG_LOOP;
+      if (P.H > 0) {
+        const int E = P.d + (loops ? 1 : 0);
+        j->e_max = std::max(j->e_max, E);
+        j->ntl_max = std::max(j->ntl_max, std::min(P.n + (loops ? 2 : 1), E + 1));
+        j->any_loop |= loops;
+      }
+    }
     D.T_eval = P.T_eval;
     D.gamma_off = gamma_stride ? (int64_t)b * gamma_stride : 0;
     D.unit_begin = unit;
@@ -311,7 +347,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     uint64_t R = 1;
     for (int h = 0; h < P.H; ++h) { upool.push_back(R); R *= (uint64_t)(P.eta[h] + 1); }
     D.mat_off = cpool_words;
-    cpool_words += (int64_t)P.d * P.d + 2 * P.d + 2;
+    cpool_words += (int64_t)(P.d + 1) * (P.d + 1) + 2 * P.d + 2;  // v1: Ct|uh|v|beta; v2: E x E
   }
   j->units = unit;
   j->plan_bytes = j->descs.size() * sizeof(PatDesc) + ipool.size() * 4 + dpool.size() * 8 +
@@ -327,8 +363,6 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   if (e == cudaSuccess) e = cudaMalloc(&j->d_counter, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&j->d_out, std::max(1, batch) * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc(&j->d_abs, std::max(1, batch) * sizeof(double));
-  const size_t gamma_rows = gamma_stride ? (size_t)batch : 1;
-  const size_t gamma_len = gamma_stride ? (size_t)batch * gamma_stride : (size_t)kdim;
   if (on_device) {
     j->own_inputs = false;
     j->d_A = (double2 *)A;
@@ -341,16 +375,22 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     if (e == cudaSuccess && gamma_len > 0)
       e = cudaMemcpy(j->d_gamma, gamma, gamma_len * sizeof(double2), cudaMemcpyHostToDevice);
   }
-  (void)gamma_rows;
-  if (e == cudaSuccess) e = launch_prep(j->dev(), j->d_max, 0);
+  j->variant = g_ctx.variant ? g_ctx.variant : choose_variant(j->e_max, j->n_max);
+  if (j->variant == 2 && !v2_supported(j->e_max, j->n_max)) j->variant = 1;
+  if (e == cudaSuccess) e = (j->variant == 2) ? launch_prep_v2(j->dev(), 0) : launch_prep(j->dev(), j->d_max, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     job_free(j);
     return fail(LHAF_E_CUDA, "job setup: %s", cudaGetErrorString(e));
   }
-  j->variant = g_ctx.variant ? g_ctx.variant : choose_variant(j->d_max, j->n_max);
   *out = j;
   return LHAF_OK;
+}
+
+static cudaError_t run_sieve(lhaf_job *j, uint64_t b, uint64_t e, cudaStream_t st) {
+  if (j->variant == 2)
+    return launch_sieve_v2(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st);
+  return launch_sieve(j->dev(), j->variant, j->d_max, j->n_max, b, e, g_ctx.num_sms, st);
 }
 
 static void shard(uint64_t units, uint64_t r, uint64_t R, uint64_t &b, uint64_t &e) {
@@ -377,7 +417,7 @@ static lhaf_status evaluate(lhaf_job *j, double *out_host, double *out_dev, cuda
   uint64_t b, e;
   rank_units(j->units, b, e);
   CUDA_TRY(cudaMemsetAsync(j->d_partials, 0, std::max<uint64_t>(1, j->units) * sizeof(Partial), st));
-  CUDA_TRY(launch_sieve(j->dev(), j->variant, j->d_max, j->n_max, b, e, g_ctx.num_sms, st));
+  CUDA_TRY(run_sieve(j, b, e, st));
   lhaf_status s = job_allreduce_impl(j, st);
   if (s != LHAF_OK) return s;
   double2 *dst = out_dev ? (double2 *)out_dev : j->d_out;
@@ -440,7 +480,7 @@ lhaf_status lhaf_set_device(int32_t device) {
 }
 
 lhaf_status lhaf_set_kernel(int32_t variant) {
-  if (variant < 0 || variant > 1) return fail(LHAF_E_ARG, "unknown kernel variant %d", variant);
+  if (variant < 0 || variant > 2) return fail(LHAF_E_ARG, "unknown kernel variant %d", variant);
   g_ctx.variant = variant;
   return LHAF_OK;
 }
@@ -459,7 +499,12 @@ lhaf_status lhaf_job_info_get(const lhaf_job *j, lhaf_job_info *info) {
   // model flops of the first non-empty pattern (batches here are uniform in d)
   info->flops_per_term_model = 0.0;
   for (const auto &D : j->descs)
-    if (D.d > 0) { info->flops_per_term_model = flops_per_term(j->variant, D.d, D.n, true); break; }
+    if (D.d > 0) {
+      const bool lp = (D.flags & FLAG_LOOP) != 0;
+      info->flops_per_term_model = (j->variant == 2) ? v2_flops_per_term(D.d, D.n, lp)
+                                                     : flops_per_term(j->variant, D.d, D.n, true);
+      break;
+    }
   return LHAF_OK;
 }
 
@@ -478,8 +523,7 @@ lhaf_status lhaf_job_run(lhaf_job *j, uint64_t ub, uint64_t ue, void *stream) {
                                             (unsigned long long)j->units);
   lhaf_status s = ensure_device();
   if (s != LHAF_OK) return s;
-  CUDA_TRY(launch_sieve(j->dev(), j->variant, j->d_max, j->n_max, ub, ue, g_ctx.num_sms,
-                        (cudaStream_t)stream));
+  CUDA_TRY(run_sieve(j, ub, ue, (cudaStream_t)stream));
   return LHAF_OK;
 }
 
@@ -525,7 +569,11 @@ lhaf_status lhaf_job_terms(lhaf_job *j, const uint64_t *t, int32_t nt, double *g
   CUDA_TRY(cudaMalloc(&dt, std::max(1, nt) * sizeof(uint64_t)));
   CUDA_TRY(cudaMalloc(&dg, std::max(1, nt) * sizeof(double2)));
   cudaError_t e = cudaMemcpy(dt, t, nt * sizeof(uint64_t), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = launch_terms(j->dev(), j->variant, j->descs[0].d, j->descs[0].n, dt, nt, dg, 0);
+  if (e == cudaSuccess) {
+    const PatDesc &D0 = j->descs[0];
+    e = (j->variant == 2) ? launch_terms_v2(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
+                          : launch_terms(j->dev(), j->variant, D0.d, D0.n, dt, nt, dg, 0);
+  }
   if (e == cudaSuccess) e = cudaMemcpy(g_out, dg, nt * sizeof(double2), cudaMemcpyDeviceToHost);
   cudaFree(dt);
   cudaFree(dg);

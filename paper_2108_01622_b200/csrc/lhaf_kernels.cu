@@ -14,111 +14,11 @@
 // Variants: 1 = generic warp-per-term, matrix in shared memory (this file, "v1").
 #include <cstdio>
 #include <cuda_runtime.h>
-#include "lhaf_internal.h"
+#include "lhaf_device.cuh"
 
 namespace lhaf {
 
-#define FULL 0xffffffffu
-
-// ---------------------------------------------------------------- complex helpers
-__device__ __forceinline__ double2 c0() { return make_double2(0.0, 0.0); }
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-// acc + a*b
-__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
-  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y);
-  return acc;
-}
-// acc - a*b
-__device__ __forceinline__ double2 cfms(double2 a, double2 b, double2 acc) {
-  acc.x = fma(-a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
-  acc.y = fma(-a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
-  return acc;
-}
-// acc + conj(a)*b
-__device__ __forceinline__ double2 cfma_cj(double2 a, double2 b, double2 acc) {
-  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
-  return acc;
-}
-// acc - a*conj(b)
-__device__ __forceinline__ double2 cfms_jc(double2 a, double2 b, double2 acc) {
-  acc.x = fma(-a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
-  return acc;
-}
-__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-
-// xor-butterfly sums: every lane ends with bit-identical values (IEEE + is commutative).
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(FULL, v, m);
-  return v;
-}
-__device__ __forceinline__ double2 warp_sum2(double2 v) {
-#pragma unroll
-  for (int m = 16; m; m >>= 1) {
-    v.x += __shfl_xor_sync(FULL, v.x, m);
-    v.y += __shfl_xor_sync(FULL, v.y, m);
-  }
-  return v;
-}
-
-// ---------------------------------------------------------------- double-double
-__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
-  s = a + b;
-  double bb = s - a;
-  e = (a - (s - bb)) + (b - bb);
-}
-__device__ __forceinline__ void dd_add(double &hi, double &lo, double x) {
-  double s, e;
-  two_sum(hi, x, s, e);
-  e += lo;
-  hi = s + e;
-  lo = e - (hi - s);
-}
-__device__ __forceinline__ void dd_add_dd(double &hi, double &lo, double xh, double xl) {
-  double s, e;
-  two_sum(hi, xh, s, e);
-  e += lo + xl;
-  hi = s + e;
-  lo = e - (hi - s);
-}
-
-// ---------------------------------------------------------------- plan helpers
-__device__ __forceinline__ int find_pattern(const JobDev &J, uint64_t u) {
-  int lo = 0, hi = J.npat - 1;
-  while (lo < hi) {  // largest p with unit_begin <= u
-    int mid = (lo + hi + 1) >> 1;
-    if (J.descs[mid].unit_begin <= u) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-// a4: decode on lanes h < H.  Returns sign; writes w[h] to smem; weight broadcast.
-__device__ __forceinline__ int decode_term(const PatDesc &P, const JobDev &J, uint64_t t, int lane,
-                                           int *w_s, double &weight) {
-  const int H = P.H;
-  int kd = 0;
-  double fac = 1.0;
-  if (lane < H) {
-    const int e = J.ipool[P.eta_off + lane];
-    const uint64_t R = J.upool[P.radix_off + lane];
-    kd = (int)((t / R) % (uint64_t)(e + 1));
-    w_s[lane] = e - 2 * kd;
-    fac = J.dpool[P.bin_off + J.ipool[P.eta_off + H + lane] + kd];
-  }
-  const unsigned odd = __ballot_sync(FULL, (lane < H) && (kd & 1));
-#pragma unroll
-  for (int m = 16; m; m >>= 1) fac *= __shfl_xor_sync(FULL, fac, m);
-  weight = fac;
-  __syncwarp();
-  return (__popc(odd) & 1) ? -1 : 1;
-}
+#define FULL LHAF_FULL
 
 // ================================================================ variant 1 (generic)
 struct V1Smem {
@@ -542,6 +442,6 @@ double flops_per_term(int variant, int d, int n, bool loops) {
   return 8.0 * cmac;
 }
 
-int choose_variant(int, int) { return 1; }
+int choose_variant(int e_max, int n_max) { return v2_supported(e_max, n_max) ? 2 : 1; }
 
 }  // namespace lhaf
