@@ -68,4 +68,12 @@ cudaError_t launch_terms_v2(const JobDev &job, int e, int ntl, int n, const uint
                             double2 *g_out, cudaStream_t s);
 double v2_flops_per_term(int d, int n, bool loops);
 
+// Variant 3 (lhaf_v3.cu): branch-free fused per-column body, band + trailing La Budde.
+// Uses the v2 prep kernel (bordered column-swapped B0).
+cudaError_t launch_sieve_v3(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t unit_begin,
+                            uint64_t unit_end, int num_sms, cudaStream_t s);
+cudaError_t launch_terms_v3(const JobDev &job, int e_max, int ntl_max, int n_max, const uint64_t *t,
+                            int nt, double2 *g_out, cudaStream_t s);
+double v3_flops_per_term(int d, int n, bool loops);
+
 }  // namespace lhaf

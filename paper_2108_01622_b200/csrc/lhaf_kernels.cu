@@ -442,6 +442,6 @@ double flops_per_term(int variant, int d, int n, bool loops) {
   return 8.0 * cmac;
 }
 
-int choose_variant(int e_max, int n_max) { return v2_supported(e_max, n_max) ? 2 : 1; }
+int choose_variant(int e_max, int n_max) { return v2_supported(e_max, n_max) ? 3 : 1; }
 
 }  // namespace lhaf

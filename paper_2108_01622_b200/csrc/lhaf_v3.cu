@@ -1,0 +1,527 @@
+// lhaf_v3.cu -- variant 3 of the sieve kernel: register-resident rows, Gauss-transform
+// Hessenberg reduction of the bordered matrix with a branch-free per-column body, then a
+// trailing La Budde on the band of H and the power series.  DESIGN.md "Kernel v3";
+// SURVEY 8(a) rows a4-a11.
+//
+// One "team" of 32*NW threads evaluates one sieve term at a time; a CTA holds TEAMS teams.
+//   a4  decode t -> w_h = eta_h - 2 k_h, sign (-1)^{sum k}, weight prod C(eta_h, k_h)
+//   a5  B = [[0, z^T], [y, M]] with M = C X_w, y = v, z^T = v X_w (loops present), else B = M.
+//       Row r of B lives in the registers of S threads; slot s of thread (r, par) holds column
+//       S*s + par.
+//   a6  Hessenberg reduction of B by Gauss transforms with partial pivoting, index 0 fixed
+//       (so the first step maps y -> beta e1 and carries z^T -> z^T L^{-1}: the "bordered"
+//       loop trick).  Rows and columns never move: index i gets its final Hessenberg position
+//       as a label.  Per column k one team barrier:
+//         argmax over the remaining rows -> each warp's best row is published to smem;
+//         every row then does, in ONE fused pass over all its slots,
+//             left   A[r][c] -= m_r A[p][c]          (m_r = B[r][k] / piv, 0 if r is done)
+//             right  acc     += A[r][c] B[c][k]      (B[c][k] = 0 unless c is remaining)
+//         and the new pivot column p = acc / piv is carried in registers (never stored).
+//       Columns of finished indices are left as garbage (they are multiplied by zero).
+//       Finished columns go to the band hb (H[j][j-1 .. j+NTL-2]).
+//   a7  F_j[m] = H[j][j+m] prod_{i=1..m} H[j+i][j+i-1]; trailing La Budde on the top
+//       NTL = n+2 coefficients of q_j(x) = det(x I - H[j:, j:]): c_B = q_0, c_M = q_1.
+//   a8  loop terms: lam S(lam) = 1 - c_B / c_M, S = sum_j s_j lam^j, s_j = z^T M^{j-1} y.
+//   a9  g = [lam^n] c_M^{-1/2} exp(S/2)   (the paper's f with X -> X_w, reading C4)
+//   a10 term = (-1)^{sum k} prod C(eta_h, k_h) g, double-double accumulation per work unit.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
+#include "lhaf_device.cuh"
+
+namespace lhaf {
+namespace v3 {
+
+__constant__ double c_inv[256];  // 1/m for the series recursions
+static bool g_inv_ready = false;
+
+// Warp-uniform slot index -> one register of the row (off the per-column hot path).
+template <int CS>
+__device__ __forceinline__ double2 rd_slot(const double2 (&A)[CS], int s) {
+  double2 v = c0();
+#pragma unroll
+  for (int i = 0; i < CS; ++i)
+    if (i == s) v = A[i];
+  return v;
+}
+// value of column c (uniform) of this thread's row, on all S lanes of the row
+template <int S, int CS>
+__device__ __forceinline__ double2 read_col(const double2 (&A)[CS], int c, int lane) {
+  double2 v = rd_slot<CS>(A, c / S);
+  if constexpr (S > 1) v = shfl2(v, (lane & ~(S - 1)) | (c & (S - 1)));
+  return v;
+}
+
+// Hides a value from loop-invariant code motion (per-pattern quantities are re-derived for
+// every term instead of being hoisted out of the term loop into live registers).
+__device__ __forceinline__ int opaque(int x) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
+
+template <int NW, int TEAMS>
+__device__ __forceinline__ void team_sync(int team) {
+  if constexpr (NW == 1) {
+    __syncwarp();
+  } else if constexpr (TEAMS == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(32 * NW) : "memory");
+  }
+}
+
+// Shared memory of one team (double2 words):
+//   hb   [EMAX][NTL]   band of H: [j][0] = H[j][j-1], [j][1] = H[j][j], [j][1+m] = H[j][j+m]
+//   u1   union { cand [2][NW][CC] | kb [2][RC] | keys [2][NW][2] } (reduction)
+//        union { Q [(E+1)][NTL] | Qs, Rs, Es [n+2] }                (La Budde, series)
+//   w    64 ints, then 64 doubles of column weights
+template <int S, int CS, int NW>
+struct Shape {
+  static constexpr int TS = 32 * NW, RC = TS / S, CC = S * CS;
+  static constexpr int EMAX = RC < CC ? RC : CC;
+  __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 4 * NW; }
+  __host__ __device__ static int u1_words(int E, int NTL, int n) {
+    const int lab = (E + 1) * NTL + 3 * (n + 2);
+    return red_words() > lab ? red_words() : lab;
+  }
+  __host__ __device__ static int words(int E, int NTL, int n) {
+    return E * NTL + u1_words(E, NTL, n) + 32 + 32;
+  }
+};
+
+// ================================================================ one term, one team
+template <int S, int CS, int NW, int TEAMS>
+__device__ double2 team_term(const PatDesc &P, const JobDev &J, uint64_t t, double2 *tbase,
+                             int tid, int team, int &sign, double &weight) {
+  using Sh = Shape<S, CS, NW>;
+  constexpr int RC = Sh::RC, CC = Sh::CC;
+  const int lane = tid & 31, warp = tid >> 5;
+  const bool loops = (P.flags & FLAG_LOOP) != 0;
+  const int o = opaque(loops ? 1 : 0);
+  const int H = opaque(P.H), n = opaque(P.n);
+  const int E = opaque(P.d) + o;
+  const int NTL = min(n + 1 + o, E + 1);
+  double2 *hb = tbase;
+  double2 *u1 = hb + E * NTL;
+  int *wv = reinterpret_cast<int *>(u1 + Sh::u1_words(E, NTL, n));
+  double *ww = reinterpret_cast<double *>(wv + 64);
+
+  // ---- a4: decode; ww[c] = weight of column c of B (1 for the border column)
+  if (warp == 0) {
+    sign = decode_term(P, J, t, lane, wv, weight);
+    __syncwarp();
+    for (int c = lane; c < CC; c += 32) {
+      const int j = c - o;
+      ww[c] = (c >= E) ? 0.0 : (j < 0) ? 1.0 : (double)wv[j < H ? j : j - H];
+    }
+  }
+  team_sync<NW, TEAMS>(team);
+
+  // ---- a5: rows of B = B0 diag(ww), B0 = the prep kernel's bordered column-swapped matrix
+  const int rr = tid / S, par = tid % S;
+  double2 A[CS];
+  {
+    const double2 *row = J.cpool + P.mat_off + (size_t)(rr < E ? rr : 0) * E + par;
+    const double *wp = ww + par;
+#pragma unroll
+    for (int s = 0; s < CS; ++s) {
+      double2 val = c0();
+      if (rr < E && S * s + par < E) val = cscale(row[S * s], wp[S * s]);
+      A[s] = val;
+    }
+  }
+
+  // ---- a6: Gauss-transform Hessenberg reduction, one barrier per column
+  double2 *cand = u1;                  // [2][NW][CC]
+  double2 *kbuf = cand + 2 * NW * CC;  // [2][RC]
+  double2 *keys = kbuf + 2 * RC;       // [2][NW][2]
+  int label = rr;
+  uint64_t live = (E >= 64 ? ~0ull : ((1ull << E) - 1ull)) & ~1ull;  // indices with label > k
+  double2 colv = (S == 1) ? A[0] : shfl2(A[0], lane & ~(S - 1));    // this row's B[.][k]
+  int buf = 0;
+  const int kend = E >= 2 ? E - 2 : 0;
+  for (int k = 0; k < kend; ++k) {
+    double2 *cb = cand + buf * NW * CC;
+    double2 *kb = kbuf + buf * RC;
+    double2 *yb = keys + buf * NW * 2;
+    buf ^= 1;
+    const bool candr = label > k && label < E;
+    double key = candr ? fabs(colv.x) + fabs(colv.y) : -1.0;
+    int code = label * 128 + rr;  // ties: smallest label wins
+#pragma unroll
+    for (int m = S; m < 32; m <<= 1) {
+      const double k2 = __shfl_xor_sync(LHAF_FULL, key, m);
+      const int c2 = __shfl_xor_sync(LHAF_FULL, code, m);
+      if (k2 > key || (k2 == key && c2 < code)) { key = k2; code = c2; }
+    }
+    if (par == 0) kb[rr] = candr ? colv : c0();
+    if (key >= 0.0 && code == label * 128 + rr) {  // this warp's best row publishes itself
+      double2 *dst = cb + warp * CC + par;
+#pragma unroll
+      for (int s = 0; s < CS; ++s) dst[S * s] = A[s];
+      if (par == 0) {
+        yb[2 * warp] = make_double2(key, (double)code);
+        yb[2 * warp + 1] = colv;
+      }
+    }
+    if (lane == 0 && key < 0.0) yb[2 * warp] = make_double2(-1.0, 1e9);
+    team_sync<NW, TEAMS>(team);
+
+    double bk = -1.0, bc = 2e9;
+    int wb = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const double2 kk = yb[2 * w];
+      if (kk.x > bk || (kk.x == bk && kk.y < bc)) { bk = kk.x; bc = kk.y; wb = w; }
+    }
+    const int pcode = (int)bc;
+    const int p = pcode & 127, plabel = pcode >> 7;  // pivot: physical index and label
+    const int newlabel = (rr == p) ? k + 1 : (label == k + 1 ? plabel : label);
+    // finished column k: H[label][k] for rows with label <= k + 1
+    if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL) hb[newlabel * NTL + k + 1 - newlabel] = colv;
+    live &= ~(1ull << p);
+    if (bk > 0.0) {
+      const double2 piv = yb[2 * wb + 1];
+      const double2 ip = crecip(piv);
+      const double2 m = (candr && rr != p) ? cmul(colv, ip) : c0();
+      const double2 *rp = cb + wb * CC + par;
+      const double2 *kq = kb + par;
+      // fused left + right pass; right accumulators split by component for ILP
+      double xr0 = 0, xi0 = 0, yr0 = 0, yi0 = 0, xr1 = 0, xi1 = 0, yr1 = 0, yi1 = 0;
+#pragma unroll
+      for (int s = 0; s < CS; ++s) {
+        const double2 r = rp[S * s];
+        const double2 q = kq[S * s];
+        double2 a = cfms(m, r, A[s]);
+        A[s] = a;
+        if (s & 1) {
+          xr1 = fma(a.x, q.x, xr1); xi1 = fma(a.y, q.y, xi1);
+          yr1 = fma(a.x, q.y, yr1); yi1 = fma(a.y, q.x, yi1);
+        } else {
+          xr0 = fma(a.x, q.x, xr0); xi0 = fma(a.y, q.y, xi0);
+          yr0 = fma(a.x, q.y, yr0); yi0 = fma(a.y, q.x, yi0);
+        }
+      }
+      double2 acc = make_double2((xr0 + xr1) - (xi0 + xi1), (yr0 + yr1) + (yi0 + yi1));
+#pragma unroll
+      for (int x = 1; x < S; x <<= 1) acc = cadd(acc, shfl2_xor(acc, x));
+      colv = cmul(acc, ip);
+    } else {
+      colv = read_col<S, CS>(A, p, lane);  // nothing to eliminate: column p as it stands
+    }
+    label = newlabel;
+  }
+  // the last two columns: the carried one (label kend) and the remaining live index
+  if (E >= 1) {
+    if (par == 0 && label < E && kend + 1 - label < NTL) hb[label * NTL + kend + 1 - label] = colv;
+    if (E >= 2) {
+      const int pl = __ffsll((long long)live) - 1;  // label E-1
+      const double2 cl = read_col<S, CS>(A, pl, lane);
+      if (par == 0 && label < E && E - label < NTL) hb[label * NTL + E - label] = cl;
+    }
+  }
+  team_sync<NW, TEAMS>(team);
+
+  // ---- a7: F_j[m] = H[j][j+m] prod_{i=1..m} H[j+i][j+i-1] in place; trailing La Budde
+  if (par == 0 && label < E) {
+    double2 pi = c1();
+    const int mmax = min(NTL - 2, E - 1 - label);
+    for (int m = 1; m <= mmax; ++m) {
+      pi = cmul(pi, hb[(label + m) * NTL]);
+      hb[label * NTL + 1 + m] = cmul(hb[label * NTL + 1 + m], pi);
+    }
+  }
+  team_sync<NW, TEAMS>(team);
+  double2 *Q = u1;  // [E+1][NTL]: Q[j][t] = coefficient of x^{deg q_j - t}
+  double2 g = c0();
+  if (warp == 0) {
+    for (int tt = lane; tt < NTL; tt += 32) Q[E * NTL + tt] = (tt == 0) ? c1() : c0();
+    __syncwarp();
+    for (int j = E - 1; j >= 0; --j) {
+      const double2 *q1 = Q + (j + 1) * NTL;
+      const double2 *Fj = hb + j * NTL;
+      const double2 hjj = Fj[1];
+      for (int tt = lane; tt < NTL; tt += 32) {
+        double2 v0 = c0(), v1 = c0(), v2 = c0(), v3 = c0();
+        if (tt <= E - j) {
+          v0 = q1[tt];  // zero above the degree of q_{j+1}
+          if (tt >= 1) v1 = cmul(hjj, q1[tt - 1]);
+          const int mm = min(tt - 1, E - 1 - j);
+          const double2 *qd = Q + (j + 2) * NTL + tt - 2;  // q_{j+m+1}[tt-m-1] at m = 1
+          int m = 1;
+          for (; m + 3 <= mm; m += 4) {
+            v0 = cfms(Fj[1 + m], qd[0], v0);
+            v1 = cfma(Fj[2 + m], qd[NTL - 1], v1);
+            v2 = cfma(Fj[3 + m], qd[2 * NTL - 2], v2);
+            v3 = cfma(Fj[4 + m], qd[3 * NTL - 3], v3);
+            qd += 4 * (NTL - 1);
+          }
+          for (; m <= mm; ++m, qd += NTL - 1) v0 = cfms(Fj[1 + m], qd[0], v0);
+        }
+        Q[j * NTL + tt] = csub(v0, cadd(cadd(v1, v2), v3));
+      }
+      __syncwarp();
+    }
+
+    // ---- a8/a9: series (lane m holds coefficients m, m+32, ...)
+    constexpr int NR = 5;  // n + 2 <= 160
+    const double2 *cB = Q;
+    const double2 *cM = loops ? Q + NTL : Q;
+    double2 *Qs = Q + (E + 1) * NTL;  // c_M^{-1/2}
+    double2 *Rs = Qs + (n + 2);       // (c_M - c_B) / c_M
+    double2 *Es = Rs + (n + 2);       // exp(S/2)
+    double2 qa[NR], ra[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int m = lane + 32 * r;
+      qa[r] = c0();
+      ra[r] = (loops && m <= n + 1 && m < NTL) ? csub(cM[m], cB[m]) : c0();
+    }
+    const int jmax = loops ? n + 1 : n;
+    for (int j = 0; j <= jmax; ++j) {
+      const int rj = j >> 5, lj = j & 31;
+      double2 qj = c0(), rv = c0();
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (r == rj) { qj = qa[r]; rv = ra[r]; }
+      qj = (j == 0) ? c1() : cscale(qj, -c_inv[j]);
+      qj = shfl2(qj, lj);
+      rv = shfl2(rv, lj);
+      if (lane == lj) { Qs[j] = qj; Rs[j] = rv; }
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int m = lane + 32 * r;
+        if (m > j && m <= jmax && m - j < NTL) {
+          const double2 cmj = cM[m - j];
+          if (m <= n) qa[r] = cfma(cscale(cmj, 0.5 * (double)(m + j)), qj, qa[r]);
+          if (loops) ra[r] = cfms(cmj, rv, ra[r]);
+        }
+      }
+    }
+    __syncwarp();
+    if (!loops) {
+      g = Qs[n];
+    } else {
+      double2 ea[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) ea[r] = c0();
+      for (int i = 0; i <= n; ++i) {
+        const int ri = i >> 5, li = i & 31;
+        double2 ei = c0();
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          if (r == ri) ei = ea[r];
+        ei = (i == 0) ? c1() : cscale(ei, c_inv[i]);
+        ei = shfl2(ei, li);
+        if (lane == li) Es[i] = ei;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const int m = lane + 32 * r;
+          if (m > i && m <= n) ea[r] = cfma(cscale(Rs[m - i + 1], 0.5 * (double)(m - i)), ei, ea[r]);
+        }
+      }
+      __syncwarp();
+      double2 gp = c0();
+      for (int m = lane; m <= n; m += 32) gp = cfma(Qs[m], Es[n - m], gp);
+      g = warp_sum2(gp);
+    }
+  }
+  team_sync<NW, TEAMS>(team);  // smem reused by the next term
+  return g;
+}
+
+// ================================================================ kernels
+template <int S, int CS, int NW, int TEAMS, int REGS>
+__global__ void __maxnreg__(REGS)
+sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
+  extern __shared__ double2 smem[];
+  __shared__ unsigned long long s_unit;
+  __shared__ double s_acc[TEAMS][6];
+  constexpr int TS = 32 * NW;
+  const int team = threadIdx.x / TS, tid = threadIdx.x % TS;
+  double2 *tbase = smem + (size_t)team * team_words;
+  for (int i = tid; i < team_words; i += TS) tbase[i] = c0();
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_unit = ubeg + atomicAdd(J.counter, 1ull);
+    __syncthreads();
+    const uint64_t u = s_unit;
+    if (u >= uend) break;
+    const PatDesc P = J.descs[find_pattern(J, u)];
+    const uint64_t tb = (u - P.unit_begin) * P.chunk;
+    const uint64_t te = min(tb + P.chunk, P.T_eval);
+    double rh = 0, rl = 0, ih = 0, il = 0, ah = 0, al = 0;
+    for (uint64_t t = tb + team; t < te; t += TEAMS) {
+      int sign = 1;
+      double weight = 1.0;
+      const double2 g = team_term<S, CS, NW, TEAMS>(P, J, t, tbase, tid, team, sign, weight);
+      if (tid == 0) {
+        const double sw = sign * weight;
+        dd_add(rh, rl, sw * g.x);
+        dd_add(ih, il, sw * g.y);
+        dd_add(ah, al, weight * hypot(g.x, g.y));
+      }
+    }
+    if (tid == 0) {
+      s_acc[team][0] = rh; s_acc[team][1] = rl; s_acc[team][2] = ih;
+      s_acc[team][3] = il; s_acc[team][4] = ah; s_acc[team][5] = al;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+      for (int w = 0; w < TEAMS; ++w) {
+        dd_add_dd(a0, a1, s_acc[w][0], s_acc[w][1]);
+        dd_add_dd(a2, a3, s_acc[w][2], s_acc[w][3]);
+        dd_add_dd(a4, a5, s_acc[w][4], s_acc[w][5]);
+      }
+      Partial q;
+      q.re_hi = a0; q.re_lo = a1; q.im_hi = a2; q.im_lo = a3; q.abs_hi = a4; q.abs_lo = a5;
+      q.pad0 = 0; q.pad1 = 0;
+      J.partials[u] = q;
+    }
+  }
+}
+
+// g(t) (unweighted) of pattern 0 for a list of term indices; one team per index.
+template <int S, int CS, int NW, int TEAMS, int REGS>
+__global__ void __maxnreg__(REGS)
+terms_v3(JobDev J, const uint64_t *ts, int nt, double2 *g_out, int team_words) {
+  extern __shared__ double2 smem[];
+  constexpr int TS = 32 * NW;
+  const int team = threadIdx.x / TS, tid = threadIdx.x % TS;
+  double2 *tbase = smem + (size_t)team * team_words;
+  for (int i = tid; i < team_words; i += TS) tbase[i] = c0();
+  __syncthreads();
+  const PatDesc P = J.descs[0];
+  for (int base = blockIdx.x * TEAMS; base < nt; base += gridDim.x * TEAMS) {
+    const int i = base + team;
+    if (i < nt) {
+      int sign;
+      double weight;
+      const double2 g = team_term<S, CS, NW, TEAMS>(P, J, ts[i], tbase, tid, team, sign, weight);
+      if (tid == 0) g_out[i] = g;
+    }
+  }
+}
+
+// ================================================================ host side
+template <int S, int CS, int NW, int TEAMS, int REGS>
+struct Inst {
+  using Sh = Shape<S, CS, NW>;
+  static constexpr int EMAX = Sh::EMAX;
+  static constexpr int THREADS = 32 * NW * TEAMS;
+  static cudaError_t sieve(const JobDev &job, int E, int NTL, int n, uint64_t ubeg, uint64_t uend,
+                           int num_sms, cudaStream_t s) {
+    const int tw = Sh::words(E, NTL, n);
+    const size_t smem = (size_t)tw * TEAMS * sizeof(double2);
+    auto *kern = sieve_v3<S, CS, NW, TEAMS, REGS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t units = uend - ubeg;
+    uint64_t grid = (uint64_t)num_sms * per_sm;
+    if (grid > units) grid = units;
+    e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw);
+    return cudaGetLastError();
+  }
+  static cudaError_t terms(const JobDev &job, int E, int NTL, int n, const uint64_t *t, int nt,
+                           double2 *g_out, cudaStream_t s) {
+    const int tw = Sh::words(E, NTL, n);
+    const size_t smem = (size_t)tw * TEAMS * sizeof(double2);
+    auto *kern = terms_v3<S, CS, NW, TEAMS, REGS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int grid = (nt + TEAMS - 1) / TEAMS;
+    if (grid > 1024) grid = 1024;
+    kern<<<grid, THREADS, smem, s>>>(job, t, nt, g_out, tw);
+    return cudaGetLastError();
+  }
+};
+
+// <S, CS, NW, TEAMS, registers per thread>.  Each SM sub-partition has 16K registers, so a
+// warp of R registers allows floor(512 / R) warps per sub-partition.
+using I9 = Inst<1, 9, 1, 4, 128>;
+using I17 = Inst<1, 17, 1, 4, 128>;
+using I25 = Inst<1, 25, 1, 4, 168>;
+using I32 = Inst<1, 32, 1, 4, 168>;
+using I48 = Inst<2, 24, 3, 1, 168>;
+using I62 = Inst<2, 31, 4, 1, 168>;
+using I64 = Inst<2, 32, 4, 1, 168>;
+
+static cudaError_t ensure_inv() {
+  if (g_inv_ready) return cudaSuccess;
+  double h[256];
+  h[0] = 0.0;
+  for (int i = 1; i < 256; ++i) h[i] = 1.0 / (double)i;
+  cudaError_t e = cudaMemcpyToSymbol(c_inv, h, sizeof h);
+  if (e == cudaSuccess) g_inv_ready = true;
+  return e;
+}
+
+}  // namespace v3
+
+cudaError_t v3_ensure_tables() { return v3::ensure_inv(); }
+
+#define LHAF_V3_DISPATCH(CALL)                  \
+  if (E <= v3::I9::EMAX) return v3::I9::CALL;   \
+  if (E <= v3::I17::EMAX) return v3::I17::CALL; \
+  if (E <= v3::I25::EMAX) return v3::I25::CALL; \
+  if (E <= v3::I32::EMAX) return v3::I32::CALL; \
+  if (E <= v3::I48::EMAX) return v3::I48::CALL; \
+  if (E <= v3::I62::EMAX) return v3::I62::CALL; \
+  if (E <= v3::I64::EMAX) return v3::I64::CALL; \
+  return cudaErrorInvalidValue;
+
+cudaError_t launch_sieve_v3(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t ubeg,
+                            uint64_t uend, int num_sms, cudaStream_t s) {
+  if (uend <= ubeg) return cudaSuccess;
+  cudaError_t e = v3::ensure_inv();
+  if (e != cudaSuccess) return e;
+  const int E = e_max;
+  LHAF_V3_DISPATCH(sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s))
+}
+
+cudaError_t launch_terms_v3(const JobDev &job, int e_max, int ntl_max, int n_max, const uint64_t *t,
+                            int nt, double2 *g_out, cudaStream_t s) {
+  if (nt <= 0) return cudaSuccess;
+  cudaError_t e = v3::ensure_inv();
+  if (e != cudaSuccess) return e;
+  const int E = e_max;
+  LHAF_V3_DISPATCH(terms(job, e_max, ntl_max, n_max, t, nt, g_out, s))
+}
+
+}  // namespace lhaf
+
+namespace lhaf {
+// Algorithmic FP64 flops of one v3 term (real flops; complex MAC = 8, complex mul = 6): the
+// useful work of the Gauss-transform Hessenberg reduction of the E x E bordered matrix, the
+// band scaling, the trailing La Budde on the top NTL coefficients, the series recursions and
+// the final product.  Work the kernel spends on finished columns is
+// not counted.
+double v3_flops_per_term(int d, int n, bool loops) {
+  const int E = d + (loops ? 1 : 0);
+  const int NTL = std::min(n + (loops ? 2 : 1), E + 1);
+  double cmac = 0.0, cmul_ = 0.0;
+  for (int k = 0; k + 2 < E; ++k) {
+    const double rem = E - k - 2;  // rows eliminated
+    cmac += rem * (E - k - 1);     // left
+    cmac += (double)E * rem;       // right
+    cmul_ += rem + 1;              // multipliers, new pivot column scaling
+  }
+  for (int j = 0; j < E; ++j) cmul_ += 2.0 * std::max(0, std::min(NTL - 2, E - 1 - j));  // F
+  for (int j = E - 1; j >= 0; --j)
+    for (int t = 0; t < NTL && t <= E - j; ++t)
+      cmac += (t >= 1 ? 1 : 0) + std::max(0, std::min(t - 1, E - 1 - j));
+  const double nn = n;
+  cmac += nn * (nn + 1) / 2.0;                                                  // c_M^{-1/2}
+  if (loops) cmac += (nn + 2) * (nn + 1) / 2.0 + nn * (nn + 1) / 2.0 + nn + 1;  // R, exp, g
+  return 8.0 * cmac + 6.0 * cmul_;
+}
+}  // namespace lhaf
