@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblhaf.so")
+# LHAF_LIB_PATH selects a diagnostic build of the same library (tools/phase_timing.py)
+LIB_PATH = os.environ.get("LHAF_LIB_PATH") or os.path.join(_HERE, "liblhaf.so")
 
 LHAF_MAX_PAIRS = 64
 LHAF_OK = 0

@@ -28,13 +28,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Compile liblhaf.so (or a diagnostic variant at `out`; LHAF_NVCC_EXTRA adds nvcc flags)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-           "-Xptxas", "-v" if verbose else "-O3", "-shared", "-o", LIB, *SOURCES,
+    extra = os.environ.get("LHAF_NVCC_EXTRA", "").split()
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", *extra,
+           "-Xptxas", "-v" if verbose else "-O3", "-shared", "-o", target, *SOURCES,
            "-I", os.path.join(ROOT, "include"), "-ldl"]
     subprocess.check_call(cmd)
+    if out is not None:
+        return target
     pkg = sys.modules.get("paper_2108_01622_b200")
     if pkg is not None and hasattr(pkg, "reload_library"):
         try:  # a stale copy already mapped in this process cannot be replaced; new processes load the new one

@@ -5,6 +5,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${1:-v2}
 export LHAF_MAX_UNITS=8388608
+export LHAF_V3_ALT=${LHAF_V3_ALT:-0}
 timeout 300 python tools/prof_run.py 4 -1776 > gpurun_out/plain_cfg4.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sieve -c 1 -o gpurun_out/prof_${TAG}_cfg4 -f \
     python tools/prof_run.py 4 -1776 > gpurun_out/ncu_cfg4.log 2>&1
