@@ -92,28 +92,24 @@ __device__ __forceinline__ void team_sync(int team) {
 // Shared memory of one team (double2 words), for a pattern with (E, NTL, n):
 //   hb   [E][NTL]       band of H: [j][0] = H[j][j-1], [j][1] = H[j][j], [j][1+m] = H[j][j+m]
 //   u1   union { cand [2][NW][CC] | kb [2][RC] | keys [2][NW] | piv [2][NW] } (reduction)
-//        union { Q [E+1][NTL] | part [2][NW][NTL] | base [2][NTL] } (La Budde)
-//   cin  [2][NTL]      c_M, c_B of the term whose series is pending
-//   ser  [3][n+2]      series accumulators Q, R, E of that term
-//   psw  [2]           (sign * weight, weight), (valid, output index) of that term
-//   csw  [1]           (sign * weight, weight) of the term being reduced
+//        union { Q [E+1][NTL] | Qs, Rs, Es [n+2] }                            (La Budde, series)
 //   w    64 ints, then 64 doubles of column weights
 template <int S, int CS, int NW>
 struct Shape {
   static constexpr int TS = 32 * NW, RC = TS / S, CC = S * CS;
   static constexpr int EMAX = RC < CC ? RC : CC;
   __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 4 * NW; }
-  __host__ __device__ static int u1_words(int E, int NTL) {
-    const int lab = (E + 1) * NTL + 2 * NW * NTL + 2 * NTL;
+  __host__ __device__ static int u1_words(int E, int NTL, int n) {
+    const int lab = (E + 1) * NTL + 3 * (n + 2);
     return red_words() > lab ? red_words() : lab;
   }
   __host__ __device__ static int words(int E, int NTL, int n) {
-    return E * NTL + u1_words(E, NTL) + 2 * NTL + 3 * (n + 2) + 3 + 32 + 32;
+    return E * NTL + u1_words(E, NTL, n) + 32 + 32;
   }
 };
 
 struct TeamMem {
-  double2 *hb, *u1, *cin, *ser, *psw, *csw;
+  double2 *hb, *u1;
   int *wv;
   double *ww;
 };
@@ -123,18 +119,14 @@ __device__ __forceinline__ TeamMem carve(double2 *b, int E, int NTL, int n) {
   using Sh = Shape<S, CS, NW>;
   TeamMem T;
   T.hb = b; b += E * NTL;
-  T.u1 = b; b += Sh::u1_words(E, NTL);
-  T.cin = b; b += 2 * NTL;
-  T.ser = b; b += 3 * (n + 2);
-  T.psw = b; b += 2;
-  T.csw = b; b += 1;
+  T.u1 = b; b += Sh::u1_words(E, NTL, n);
   T.wv = reinterpret_cast<int *>(b); b += 32;
   T.ww = reinterpret_cast<double *>(b);
   return T;
 }
 
 struct Pattern {  // per-pattern sizes (kept opaque to loop-invariant motion)
-  int H, n, E, o, NTL, nss;
+  int H, n, E, o, NTL;
   bool loops;
 };
 
@@ -146,89 +138,149 @@ __device__ __forceinline__ Pattern pattern_of(const PatDesc &P) {
   D.n = opaque(P.n);
   D.E = opaque(P.d) + D.o;
   D.NTL = min(D.n + 1 + D.o, D.E + 1);
-  const int jmax = D.loops ? D.n + 1 : D.n;
-  D.nss = jmax + 1 + (D.loops ? D.n + 1 : 0) + 1;
   return D;
 }
 
-// ---------------------------------------------------------------- series program (one warp)
-// Step s of the series of one term; the accumulators in ser turn into final values in place:
-//   s <= jmax:      Q/R sweep j = s:  m Q_m = -sum_{i=1}^{m} (m - i/2) c_i Q_{m-i}  (c = c_M),
-//                   R = (c_M - c_B) / c_M  (loops only)
-//   next n+1 steps: E sweep i:  m E_m = 1/2 sum_{j=1}^{m} j S_j E_{m-j},  S_j = R_{j+1}
-//   last step:      g = sum_m Q_m E_{n-m}  (no loops: g = Q_n); returns true with g
-__device__ __forceinline__ bool series_step(const Pattern &D, int s, const double2 *cM,
-                                            double2 *ser, int lane, double2 &g) {
-  const int n = D.n, NTL = D.NTL;
-  const int jmax = D.loops ? n + 1 : n;
-  double2 *Qa = ser, *Ra = ser + (n + 2), *Ea = ser + 2 * (n + 2);
-  if (s <= jmax) {
-    const int j = s;
-    const double2 qacc = Qa[j];
-    const double2 rj = Ra[j];
-    const double2 qj = (j == 0) ? c1() : cscale(qacc, -c_inv[j]);
-    __syncwarp();
-    if (lane == (j & 31)) Qa[j] = qj;
-    for (int m = j + 1 + ((lane - j - 1) & 31); m <= jmax && m - j < NTL; m += 32) {
-      const double2 c = cM[m - j];
-      if (m <= n) Qa[m] = cfma(cscale(c, 0.5 * (double)(m + j)), qj, Qa[m]);
-      if (D.loops) Ra[m] = cfms(c, rj, Ra[m]);
-    }
-    __syncwarp();
-    return false;
-  }
-  if (D.loops && s <= jmax + 1 + n) {
-    const int i = s - jmax - 1;
-    const double2 eacc = Ea[i];
-    const double2 ei = (i == 0) ? c1() : cscale(eacc, c_inv[i]);
-    __syncwarp();
-    if (lane == (i & 31)) Ea[i] = ei;
-    for (int m = i + 1 + ((lane - i - 1) & 31); m <= n; m += 32)
-      Ea[m] = cfma(cscale(Ra[m - i + 1], 0.5 * (double)(m - i)), ei, Ea[m]);
-    __syncwarp();
-    return false;
-  }
-  if (!D.loops) {
-    g = Qa[n];
-  } else {
-    double2 gp = c0();
-    for (int m = lane; m <= n; m += 32) gp = cfma(Qa[m], Ea[n - m], gp);
-    g = warp_sum2(gp);
+// ---------------------------------------------------------------- La Budde (one warp)
+// Trailing La Budde on the top NTL coefficients (t = distance from the leading coefficient):
+//   q_j[t] = q_{j+1}[t] - h_jj q_{j+1}[t-1] + S_j[t],
+//   S_j[t] = - sum_{m=1}^{min(t-1, E-1-j)} F_j[m] q_{j+m+1}[t-m-1]     (F_j[m] = hb[j][1+m]).
+// S_j needs only rows j+2.. (already final), so iteration j computes S_{j-1} ahead of the
+// short loop-carried chain q_{j+1} -> q_j (a shuffle and two FMAs).  Lane t holds q_{j+1}[t]
+// in registers (NRT registers per lane: NTL <= 32 NRT); rows go to Q[j][t] for the m-sums.
+template <int NRT>
+__device__ __forceinline__ void labudde(const double2 *hb, double2 *Q, int E, int NTL, int lane) {
+  double2 qn[NRT], S[NRT];
+#pragma unroll
+  for (int r = 0; r < NRT; ++r) {
+    const int t = lane + 32 * r;
+    qn[r] = (t == 0) ? c1() : c0();  // q_E = 1
+    S[r] = c0();                     // S_{E-1} = 0
+    if (t < NTL) Q[E * NTL + t] = qn[r];
   }
   __syncwarp();
-  return true;
+  for (int j = E - 1; j >= 0; --j) {
+    // S_{j-1}[t] from rows j+1 .. E (final)
+    double2 Sn[NRT];
+#pragma unroll
+    for (int r = 0; r < NRT; ++r) {
+      const int t = lane + 32 * r;
+      double2 a0 = c0(), a1 = c0(), a2 = c0(), a3 = c0();
+      if (j >= 1 && t < NTL && t <= E - j + 1) {
+        const double2 *F = hb + (j - 1) * NTL + 1;  // F_{j-1}[m] = F[m]
+        const int mm = min(t - 1, E - j);
+        const double2 *qd = Q + (j + 1) * NTL + t - 2;  // q_{j+m}[t-m-1] at m = 1
+        int m = 1;
+        for (; m + 3 <= mm; m += 4) {
+          a0 = cfma(F[m], qd[0], a0);
+          a1 = cfma(F[m + 1], qd[NTL - 1], a1);
+          a2 = cfma(F[m + 2], qd[2 * (NTL - 1)], a2);
+          a3 = cfma(F[m + 3], qd[3 * (NTL - 1)], a3);
+          qd += 4 * (NTL - 1);
+        }
+        for (; m <= mm; ++m, qd += NTL - 1) a0 = cfma(F[m], qd[0], a0);
+      }
+      Sn[r] = make_double2(-((a0.x + a1.x) + (a2.x + a3.x)), -((a0.y + a1.y) + (a2.y + a3.y)));
+    }
+    // q_j from q_{j+1} (registers) and S_j
+    const double2 h = hb[j * NTL + 1];
+    double2 shfl_last[NRT];  // q_{j+1}[32 r + 31], for lane 0 of register r + 1
+#pragma unroll
+    for (int r = 0; r < NRT; ++r) shfl_last[r] = shfl2(qn[r], 31);
+    double2 up[NRT];  // q_{j+1}[t-1]
+#pragma unroll
+    for (int r = 0; r < NRT; ++r) {
+      const double2 s = shfl2(qn[r], (lane + 31) & 31);  // all lanes shuffle (full mask)
+      up[r] = (lane != 0) ? s : (r == 0 ? c0() : shfl_last[r - 1]);
+    }
+#pragma unroll
+    for (int r = 0; r < NRT; ++r) {
+      const int t = lane + 32 * r;
+      double2 q = cadd(S[r], cfms(h, up[r], qn[r]));
+      if (t > E - j) q = c0();  // above the degree of q_j
+      qn[r] = q;
+      if (t < NTL) Q[j * NTL + t] = q;
+      S[r] = Sn[r];
+    }
+    __syncwarp();
+  }
 }
 
-// Accumulation of finished terms (lane 0 of the series warp): double-double sums of
-// sign * weight * g and of weight * |g|, or g itself into the diagnostic output.
-struct Sums {
-  double rh = 0, rl = 0, ih = 0, il = 0, ah = 0, al = 0;
-};
-
-__device__ __forceinline__ void finish_term(const TeamMem &T, const double2 &g, Sums &acc,
-                                            double2 *g_out, int lane) {
-  if (lane != 0 || T.psw[1].x == 0.0) return;
-  if (g_out) {
-    g_out[(uint64_t)T.psw[1].y] = g;
-  } else {
-    const double sw = T.psw[0].x, w = T.psw[0].y;
-    dd_add(acc.rh, acc.rl, sw * g.x);
-    dd_add(acc.ih, acc.il, sw * g.y);
-    dd_add(acc.ah, acc.al, w * hypot(g.x, g.y));
+// ---------------------------------------------------------------- series (one warp)
+// g = [lam^n] c_M^{-1/2} exp(S/2), lam S = 1 - c_B / c_M (loops), by column sweeps: lane m
+// holds the accumulators of coefficients m, m+32, ... (NR registers, n + 2 <= 32 NR):
+//   m Q_m = -sum_{i=1}^{m} (m - i/2) c_i Q_{m-i}   (c = c_M),  R = (c_M - c_B) / c_M,
+//   m E_m = 1/2 sum_{j=1}^{m} j S_j E_{m-j},  S_j = R_{j+1},  g = sum_m Q_m E_{n-m}.
+// Finished coefficients go to scratch (Qs, Rs, Es: 3 (n+2) words).
+template <int NR>
+__device__ __forceinline__ double2 series(const double2 *cM, const double2 *cB, int n, int NTL,
+                                          bool loops, double2 *scratch, int lane) {
+  double2 *Qs = scratch, *Rs = Qs + (n + 2), *Es = Rs + (n + 2);
+  double2 qa[NR], ra[NR];
+  double md[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int m = lane + 32 * r;
+    md[r] = (double)m;
+    qa[r] = c0();
+    ra[r] = (loops && m <= n + 1 && m < NTL) ? csub(cM[m], cB[m]) : c0();
   }
+  const int jmax = loops ? n + 1 : n;
+  double jd = 0.0;
+  for (int j = 0; j <= jmax; ++j, jd += 1.0) {
+    const int lj = j & 31, rj = j >> 5;
+    double2 qs = qa[0], rs = ra[0];
+#pragma unroll
+    for (int r = 1; r < NR; ++r)
+      if (rj == r) { qs = qa[r]; rs = ra[r]; }
+    double2 qj = (j == 0) ? c1() : cscale(qs, -c_inv[j]);
+    qj = shfl2(qj, lj);
+    const double2 rv = shfl2(rs, lj);
+    if (lane == lj) { Qs[j] = qj; Rs[j] = rv; }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int m = lane + 32 * r;
+      if (m > j && m <= jmax && m - j < NTL) {
+        const double2 c = cM[m - j];
+        if (m <= n) qa[r] = cfma(cscale(c, 0.5 * (md[r] + jd)), qj, qa[r]);
+        if (loops) ra[r] = cfms(c, rv, ra[r]);
+      }
+    }
+  }
+  __syncwarp();
+  if (!loops) return Qs[n];
+  double2 ea[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) ea[r] = c0();
+  double id = 0.0;
+  for (int i = 0; i <= n; ++i, id += 1.0) {
+    const int li = i & 31, ri = i >> 5;
+    double2 es = ea[0];
+#pragma unroll
+    for (int r = 1; r < NR; ++r)
+      if (ri == r) es = ea[r];
+    double2 ei = (i == 0) ? c1() : cscale(es, c_inv[i]);
+    ei = shfl2(ei, li);
+    if (lane == li) Es[i] = ei;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int m = lane + 32 * r;
+      if (m > i && m <= n) ea[r] = cfma(cscale(Rs[m - i + 1], 0.5 * (md[r] - id)), ei, ea[r]);
+    }
+  }
+  __syncwarp();
+  double2 gp = c0();
+  for (int m = lane; m <= n; m += 32) gp = cfma(Qs[m], Es[n - m], gp);
+  return warp_sum2(gp);
 }
 
 // ================================================================ one term, one team
-// Reduces term t (valid == false: a duplicate term whose result is discarded) and hands its
-// characteristic polynomials to the series pipeline.  ss = next series step of the pending
-// term (== nss: nothing pending).
+// g(t) of one term (valid in warp 0 of the team); sign and weight from the decode (warp 0).
 template <int S, int CS, int NW, int TEAMS>
-__device__ void team_term(const PatDesc &P, const Pattern &D, const JobDev &J, uint64_t t,
-                          bool valid, uint64_t out_idx, const TeamMem &T, int tid, int team,
-                          int &ss, Sums &acc, double2 *g_out) {
+__device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J, uint64_t t,
+                             const TeamMem &T, int tid, int team, int &sign, double &weight) {
   using Sh = Shape<S, CS, NW>;
   constexpr int RC = Sh::RC, CC = Sh::CC;
-  constexpr int SW = NW - 1;  // the series warp
   const int lane = tid & 31, warp = tid >> 5;
   const int H = D.H, n = D.n, E = D.E, o = D.o, NTL = D.NTL;
   const bool loops = D.loops;
@@ -239,14 +291,12 @@ __device__ void team_term(const PatDesc &P, const Pattern &D, const JobDev &J, u
 #endif
   // ---- a4: decode; ww[c] = weight of column c of B (1 for the border column)
   if (warp == 0) {
-    double weight;
-    const int sign = decode_term(P, J, t, lane, T.wv, weight);
+    sign = decode_term(P, J, t, lane, T.wv, weight);
     __syncwarp();
     for (int c = lane; c < CC; c += 32) {
       const int j = c - o;
       T.ww[c] = (c >= E) ? 0.0 : (j < 0) ? 1.0 : (double)T.wv[j < H ? j : j - H];
     }
-    if (lane == 0) T.csw[0] = make_double2(sign * weight, weight);
   }
   team_sync<NW, TEAMS>(team);
 
@@ -274,7 +324,6 @@ __device__ void team_term(const PatDesc &P, const Pattern &D, const JobDev &J, u
   double2 colv = (S == 1) ? A[0] : shfl2(A[0], lane & ~(S - 1));    // this row's B[.][k]
   int buf = 0;
   const int kend = E >= 2 ? E - 2 : 0;
-  const int per_k = kend > 0 ? (D.nss + kend - 1) / kend : D.nss;
   for (int k = 0; k < kend; ++k) {
     double2 *cb = cand + buf * NW * CC;
     double2 *kb = kbuf + buf * RC;
@@ -301,13 +350,6 @@ __device__ void team_term(const PatDesc &P, const Pattern &D, const JobDev &J, u
       }
     }
     if (lane == 0) yk[4 * warp] = wkey;
-    // the pending term's series advances in the shadow of this column
-    if (warp == SW) {
-      for (int x = 0; x < per_k && ss < D.nss; ++x, ++ss) {
-        double2 g;
-        if (series_step(D, ss, T.cin, T.ser, lane, g)) finish_term(T, g, acc, g_out, lane);
-      }
-    }
     team_sync<NW, TEAMS>(team);
 
     unsigned bkey = 0u;
@@ -363,13 +405,6 @@ __device__ void team_term(const PatDesc &P, const Pattern &D, const JobDev &J, u
       if (par == 0 && label < E && E - label < NTL) hb[label * NTL + E - label] = cl;
     }
   }
-  // the pending series must be complete before its buffers are reused (E tiny)
-  if (warp == SW) {
-    for (; ss < D.nss; ++ss) {
-      double2 g;
-      if (series_step(D, ss, T.cin, T.ser, lane, g)) finish_term(T, g, acc, g_out, lane);
-    }
-  }
   team_sync<NW, TEAMS>(team);
   LHAF_PHASE(1)
 
@@ -382,100 +417,26 @@ __device__ void team_term(const PatDesc &P, const Pattern &D, const JobDev &J, u
       hb[label * NTL + 1 + m] = cmul(hb[label * NTL + 1 + m], pi);
     }
   }
-  double2 *Q = T.u1;                    // [E+1][NTL]: Q[j][t] = coefficient of x^{deg q_j - t}
-  double2 *part = Q + (E + 1) * NTL;    // [2][NW][NTL] partial m-sums
-  double2 *base = part + 2 * NW * NTL;  // [2][NTL] q_{j+1}[t] - H[j][j] q_{j+1}[t-1]
-  if (warp == 0)
-    for (int tt = lane; tt < NTL; tt += 32) Q[E * NTL + tt] = (tt == 0) ? c1() : c0();
   team_sync<NW, TEAMS>(team);
   LHAF_PHASE(2)
-
-  // trailing La Budde: q_j = base_j - sum_w part_j[w]; warp w sums the m = 1 + w (mod NW)
-  // terms of q_j[t] = q_{j+1}[t] - h_jj q_{j+1}[t-1] - sum_{m=1}^{min(t-1, E-1-j)} F_j[m]
-  // q_{j+m+1}[t-m-1]; warp 0 finalizes row j+1 at the start of iteration j.
-  for (int j = E - 1; j >= 0; --j) {
-    const double2 *Fj = hb + j * NTL;
-    if (warp == 0) {
-      if (j + 1 < E) {
-        const double2 *bp = base + ((j + 1) & 1) * NTL;
-        const double2 *pp = part + ((j + 1) & 1) * NW * NTL;
-        for (int tt = lane; tt < NTL; tt += 32) {
-          double2 v = bp[tt];
-#pragma unroll
-          for (int w = 0; w < NW; ++w) v = csub(v, pp[w * NTL + tt]);
-          Q[(j + 1) * NTL + tt] = v;
-        }
-        __syncwarp();
-      }
-      const double2 *q1 = Q + (j + 1) * NTL;
-      const double2 hjj = Fj[1];
-      for (int tt = lane; tt < NTL; tt += 32) {
-        double2 v = c0();
-        if (tt <= E - j) {
-          v = q1[tt];  // zero above the degree of q_{j+1}
-          if (tt >= 1) v = cfms(hjj, q1[tt - 1], v);
-        }
-        base[(j & 1) * NTL + tt] = v;
-      }
-    }
-    double2 *pw = part + ((j & 1) * NW + warp) * NTL;
-    for (int tt = lane; tt < NTL; tt += 32) {
-      double2 v0 = c0(), v1 = c0();
-      if (tt <= E - j) {
-        const int mm = min(tt - 1, E - 1 - j);
-        int m = 1 + warp;
-        const double2 *qd = Q + (j + 1 + m) * NTL + tt - m - 1;  // q_{j+m+1}[tt-m-1]
-        for (; m + NW <= mm; m += 2 * NW) {
-          v0 = cfma(Fj[1 + m], qd[0], v0);
-          v1 = cfma(Fj[1 + m + NW], qd[NW * (NTL - 1)], v1);
-          qd += 2 * NW * (NTL - 1);
-        }
-        if (m <= mm) v0 = cfma(Fj[1 + m], qd[0], v0);
-      }
-      pw[tt] = cadd(v0, v1);
-    }
-    team_sync<NW, TEAMS>(team);
-  }
-  LHAF_PHASE(3)
-
-  // ---- hand the polynomials to the series pipeline: c_M = q_1, c_B = q_0
-  if (warp == SW) {
-    const double2 *bp = base;  // j = 0 wrote parity 0
-    const double2 *pp = part;
-    const double2 *cM = Q + NTL;
-    for (int tt = lane; tt < NTL; tt += 32) {
-      double2 q0 = bp[tt];
-#pragma unroll
-      for (int w = 0; w < NW; ++w) q0 = csub(q0, pp[w * NTL + tt]);
-      T.cin[NTL + tt] = q0;                  // c_B
-      T.cin[tt] = loops ? cM[tt] : q0;       // c_M
-    }
-    __syncwarp();
-    double2 *Qa = T.ser, *Ra = T.ser + (n + 2), *Ea = T.ser + 2 * (n + 2);
-    for (int m = lane; m < n + 2; m += 32) {
-      Qa[m] = c0();
-      Ea[m] = c0();
-      Ra[m] = (loops && m < NTL) ? csub(T.cin[m], T.cin[NTL + m]) : c0();
-    }
-    if (lane == 0) {
-      T.psw[0] = T.csw[0];
-      T.psw[1] = make_double2(valid ? 1.0 : 0.0, (double)out_idx);
-    }
-    __syncwarp();
-    ss = 0;
+  double2 g = c0();
+  if (warp == 0) {
+    double2 *Q = T.u1;  // [E+1][NTL]: Q[j][t] = coefficient of x^{deg q_j - t}
+    if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
+    else labudde<2>(hb, Q, E, NTL, lane);
+    LHAF_PHASE(3)
+    // ---- a8/a9: series from c_B = q_0, c_M = q_1 (loops) or c_M = q_0
+    const double2 *cB = Q;
+    const double2 *cM = loops ? Q + NTL : Q;
+    double2 *scr = Q + (E + 1) * NTL;
+    if (n + 2 <= 32) g = series<1>(cM, cB, n, NTL, loops, scr, lane);
+    else if (n + 2 <= 64) g = series<2>(cM, cB, n, NTL, loops, scr, lane);
+    else g = series<5>(cM, cB, n, NTL, loops, scr, lane);
   }
   LHAF_PHASE(4)
   team_sync<NW, TEAMS>(team);  // smem reused by the next term
   LHAF_PHASE(5)
-}
-
-// the series of the last term of a work unit (series warp only)
-__device__ __forceinline__ void drain_series(const Pattern &D, const TeamMem &T, int &ss,
-                                             Sums &acc, double2 *g_out, int lane) {
-  for (; ss < D.nss; ++ss) {
-    double2 g;
-    if (series_step(D, ss, T.cin, T.ser, lane, g)) finish_term(T, g, acc, g_out, lane);
-  }
+  return g;
 }
 
 // ================================================================ kernels
@@ -487,7 +448,6 @@ sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
   __shared__ double s_acc[TEAMS][6];
   constexpr int TS = 32 * NW;
   const int team = threadIdx.x / TS, tid = threadIdx.x % TS;
-  const int lane = tid & 31, warp = tid >> 5;
   double2 *tbase = smem + (size_t)team * team_words;
   for (int i = tid; i < team_words; i += TS) tbase[i] = c0();
   for (;;) {
@@ -501,20 +461,21 @@ sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
     const TeamMem T = carve<S, CS, NW>(tbase, D.E, D.NTL, D.n);
     const uint64_t tb = (u - P.unit_begin) * P.chunk;
     const uint64_t te = min(tb + P.chunk, P.T_eval);
-    Sums acc;
-    int ss = D.nss;  // nothing pending
-    // every team runs the same number of terms (duplicates of tb are discarded)
-    const uint64_t per_team = (te - tb + TEAMS - 1) / TEAMS;
-    for (uint64_t i = 0; i < per_team; ++i) {
-      const uint64_t t = tb + i * TEAMS + team;
-      const bool valid = t < te;
-      team_term<S, CS, NW, TEAMS>(P, D, J, valid ? t : tb, valid, 0, T, tid, team, ss, acc,
-                                  nullptr);
+    double rh = 0, rl = 0, ih = 0, il = 0, ah = 0, al = 0;
+    for (uint64_t t = tb + team; t < te; t += TEAMS) {
+      int sign = 1;
+      double weight = 1.0;
+      const double2 g = team_term<S, CS, NW, TEAMS>(P, D, J, t, T, tid, team, sign, weight);
+      if (tid == 0) {
+        const double sw = sign * weight;
+        dd_add(rh, rl, sw * g.x);
+        dd_add(ih, il, sw * g.y);
+        dd_add(ah, al, weight * hypot(g.x, g.y));
+      }
     }
-    if (warp == NW - 1) drain_series(D, T, ss, acc, nullptr, lane);
-    if (warp == NW - 1 && lane == 0) {
-      s_acc[team][0] = acc.rh; s_acc[team][1] = acc.rl; s_acc[team][2] = acc.ih;
-      s_acc[team][3] = acc.il; s_acc[team][4] = acc.ah; s_acc[team][5] = acc.al;
+    if (tid == 0) {
+      s_acc[team][0] = rh; s_acc[team][1] = rl; s_acc[team][2] = ih;
+      s_acc[team][3] = il; s_acc[team][4] = ah; s_acc[team][5] = al;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -532,30 +493,28 @@ sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
   }
 }
 
-// g(t) (unweighted) of pattern 0 for a list of term indices; each team takes a contiguous
-// slice of the list.
+// g(t) (unweighted) of pattern 0 for a list of term indices; one team per index.
 template <int S, int CS, int NW, int TEAMS, int REGS>
 __global__ void __maxnreg__(REGS)
 terms_v3(JobDev J, const uint64_t *ts, int nt, double2 *g_out, int team_words) {
   extern __shared__ double2 smem[];
   constexpr int TS = 32 * NW;
   const int team = threadIdx.x / TS, tid = threadIdx.x % TS;
-  const int lane = tid & 31, warp = tid >> 5;
   double2 *tbase = smem + (size_t)team * team_words;
   for (int i = tid; i < team_words; i += TS) tbase[i] = c0();
   __syncthreads();
   const PatDesc P = J.descs[0];
   const Pattern D = pattern_of(P);
   const TeamMem T = carve<S, CS, NW>(tbase, D.E, D.NTL, D.n);
-  const int nteams = gridDim.x * TEAMS;
-  const int gteam = blockIdx.x * TEAMS + team;
-  const int per = (nt + nteams - 1) / nteams;
-  const int b = gteam * per, e = min(nt, b + per);
-  Sums acc;
-  int ss = D.nss;
-  for (int i = b; i < e; ++i)
-    team_term<S, CS, NW, TEAMS>(P, D, J, ts[i], true, (uint64_t)i, T, tid, team, ss, acc, g_out);
-  if (warp == NW - 1) drain_series(D, T, ss, acc, g_out, lane);
+  for (int base = blockIdx.x * TEAMS; base < nt; base += gridDim.x * TEAMS) {
+    const int i = base + team;
+    if (i < nt) {
+      int sign;
+      double weight;
+      const double2 g = team_term<S, CS, NW, TEAMS>(P, D, J, ts[i], T, tid, team, sign, weight);
+      if (tid == 0) g_out[i] = g;
+    }
+  }
 }
 
 // ================================================================ host side
