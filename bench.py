@@ -6,9 +6,10 @@ Workload (default `--workload cfg4`): BASELINE.json config 4, the n = 60 loop ha
 2^29 evaluated sieve terms).  One "step" is one pass of the whole hot path (S8(a) a4-a12:
 decode, scale, Hessenberg, La Budde, loop terms, series, compensated accumulate, all-reduce,
 finalize) over one fixed slice of the lhaf's work units; the lhaf is cut into `--slices`
-(default 32) contiguous slices, so K = 32 timed steps evaluate the whole loop hafnian once
-and `s_per_lhaf` is then measured, not extrapolated.  Other workloads: cfg2 (the 4096-pattern
-batch, one step = the whole batch), cfg3 (n = 40 collision-heavy lhaf), cfg5 (mixed state).
+(default 64, 2^23 terms and 2048 work units per step) contiguous slices; `--steps 64`
+evaluates the whole loop hafnian once (then `s_per_lhaf` is measured, not extrapolated).  Other workloads:
+cfg2 (the 4096-pattern batch, one step = the whole batch), cfg3 (n = 40 collision-heavy lhaf),
+cfg5 (mixed state).
 
 Timing: W untimed warm-up steps; then barrier + cuda synchronize, CUDA events on the launch
 stream around exactly K steps, synchronize + barrier; max over ranks.  Between steps a 256 MiB
@@ -43,10 +44,10 @@ sys.path.insert(0, ROOT)
 import gbs_inputs as G  # noqa: E402
 
 WORKLOADS = {
-    "cfg4": dict(cfg=4, slices=32, desc="BASELINE config 4: single n=60 loop hafnian, m=100 Haar, tanh r=0.9, gamma sigma=0.1, 60 distinct modes, 2^29 evaluated terms at d=60"),
+    "cfg4": dict(cfg=4, slices=64, desc="BASELINE config 4: single n=60 loop hafnian, m=100 Haar, tanh r=0.9, gamma sigma=0.1, 60 distinct modes, 2^29 evaluated terms at d=60"),
     "cfg2": dict(cfg=2, slices=1, desc="BASELINE config 2: batch of 4096 loop hafnians, N=24 distinct modes of m=50, 2^11 evaluated terms each at d=24"),
     "cfg3": dict(cfg=3, slices=1, desc="BASELINE config 3: n=40 collision-heavy loop hafnian, 16 modes of m=100, gamma=0"),
-    "cfg5": dict(cfg=5, slices=64, desc="BASELINE config 5: mixed-state lhaf, 36 photons over 24 modes, eta=0.3, 2k=200, natural pairing, d=48"),
+    "cfg5": dict(cfg=5, slices=128, desc="BASELINE config 5: mixed-state lhaf, 36 photons over 24 modes, eta=0.3, 2k=200, natural pairing, d=48"),
 }
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
 
@@ -186,7 +187,7 @@ def main():
     w = WORKLOADS[args.workload]
     slices = args.slices or w["slices"]
     if args.steps is None:
-        args.steps = slices if slices > 1 else 5
+        args.steps = 5
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -276,7 +277,7 @@ def main():
     value = total_terms / (ms * 1e-3)
     result = out_dev.cpu().numpy()
     full_cover = args.steps >= slices
-    s_per_lhaf = (ms * 1e-3 * slices / args.steps) if job.info.batch == 1 else None
+    s_per_lhaf = (job.terms / value) if job.info.batch == 1 else None
 
     # roofline: algorithmic FP64 flops per launch / launch duration, vs measured DFMA peak
     flops_term = job.info.flops_per_term_model
@@ -294,7 +295,8 @@ def main():
         except Exception:
             pass
 
-    # e2e: the public C-ABI call with host buffers (whole loop hafnian / whole batch)
+    # e2e: the public C-ABI with host buffers, every step: job create (H2D of A, gamma, plan),
+    # run over the step's slice, finalize (D2H of the result); the batch: lhaf_rpt_batch
     e2e = None
     if not args.no_e2e:
         A = np.ascontiguousarray(cfg["A"])
@@ -302,23 +304,34 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        e2e_terms = 0.0
         t0 = time.perf_counter()
-        if cfg["mixed"]:
-            v = L.lhaf_rpt_mixed(A, gm, reps)
-        elif reps.ndim == 2:
-            v = L.lhaf_rpt_batch(A, gm, reps)
-        else:
-            v = L.lhaf_rpt(A, gm, reps)
+        for s in range(args.steps):
+            if reps.ndim == 2:
+                v = L.lhaf_rpt_batch(A, gm, reps)
+                e2e_terms += job.terms * (rank == 0)
+            else:
+                jb = L.Job(A, gm, reps, mixed=cfg["mixed"])
+                ub, ue = slice_units(s)
+                jb.reset()
+                jb.run(ub, ue)
+                jb.allreduce()
+                v = jb.finalize()
+                e2e_terms += (ue - ub) * terms_per_unit
+                jb.close()
+        torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t[0])
+            t = torch.tensor([dt, e2e_terms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+            tt2 = t[1:].clone()
+            dist.all_reduce(tt2)
+            dt, e2e_terms = float(t[0]), float(tt2[0])
         h2d = A.nbytes + gm.nbytes + int(job.info.h2d_plan_bytes)
         d2h = 16 * job.info.batch
-        e2e = {"value": job.terms / dt, "unit": "terms/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "s_per_call": dt,
-               "call": "lhaf_rpt_mixed" if cfg["mixed"] else ("lhaf_rpt_batch" if reps.ndim == 2 else "lhaf_rpt"),
+        e2e = {"value": e2e_terms / dt, "unit": "terms/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "s_per_step": dt / args.steps,
+               "call": "lhaf_rpt_batch" if reps.ndim == 2 else "lhaf_job_create/run/allreduce/finalize (host buffers)",
                "result_first": [complex(np.atleast_1d(v)[0]).real, complex(np.atleast_1d(v)[0]).imag]}
 
     cpu = None

@@ -193,13 +193,14 @@ lhaf_status check_symmetric(const double *A, int m) {
 }
 
 uint64_t chunk_for(uint64_t T_eval) {
-  // Terms per work unit: T_eval split into at most 32768 units of >= 64 terms (independent
-  // of the number of ranks, so results are bit-identical for any rank count).  LHAF_MAX_UNITS
+  // Terms per work unit: T_eval split into at most 2^17 units of >= 64 terms (independent
+  // of the number of ranks, so results are bit-identical for any rank count; small enough
+  // units that a 1/64 slice of a 2^29-term lhaf still spreads over every SM).  LHAF_MAX_UNITS
   // overrides the unit cap (profiling runs use small units to fill the GPU with few terms).
   static const uint64_t max_units = [] {
     const char *e = getenv("LHAF_MAX_UNITS");
     const uint64_t v = e ? strtoull(e, nullptr, 10) : 0;
-    return v ? v : (uint64_t)32768;
+    return v ? v : (uint64_t)131072;
   }();
   const uint64_t min_chunk = 64;
   uint64_t c = (T_eval + max_units - 1) / max_units;
