@@ -92,7 +92,7 @@ __device__ __forceinline__ void team_sync(int team) {
 // Shared memory of one team (double2 words), for a pattern with (E, NTL, n):
 //   hb   [E][NTL]       band of H: [j][0] = H[j][j-1], [j][1] = H[j][j], [j][1+m] = H[j][j+m]
 //   u1   union { cand [2][NW][CC] | kb [2][RC] | keys [2][NW] | piv [2][NW] } (reduction)
-//        union { Q [E+1][NTL] | Qs, Rs, Es [n+2] }                            (La Budde, series)
+//        union { Q [E+1][NTL] | Qs, Rs, Es [n+2] | part [2][NW][NTL] }         (La Budde, series)
 //   w    64 ints, then 64 doubles of column weights
 template <int S, int CS, int NW>
 struct Shape {
@@ -100,7 +100,7 @@ struct Shape {
   static constexpr int EMAX = RC < CC ? RC : CC;
   __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 4 * NW; }
   __host__ __device__ static int u1_words(int E, int NTL, int n) {
-    const int lab = (E + 1) * NTL + 3 * (n + 2);
+    const int lab = (E + 1) * NTL + 3 * (n + 2) + 2 * NW * NTL;
     return red_words() > lab ? red_words() : lab;
   }
   __host__ __device__ static int words(int E, int NTL, int n) {
@@ -203,6 +203,70 @@ __device__ __forceinline__ void labudde(const double2 *hb, double2 *Q, int E, in
       S[r] = Sn[r];
     }
     __syncwarp();
+  }
+}
+
+// Team version: warp w sums the m = 1 + w (mod NW) part of S_{j-1} into part[j&1][w][t];
+// warp 0 keeps q_{j+1} in registers and forms q_j = q_{j+1} - h q_{j+1}[t-1] - sum_w part;
+// one team barrier per row.
+template <int NRT, int NW, int TEAMS>
+__device__ __forceinline__ void labudde_team(const double2 *hb, double2 *Q, double2 *part, int E,
+                                             int NTL, int warp, int lane, int team) {
+  double2 qn[NRT];
+#pragma unroll
+  for (int r = 0; r < NRT; ++r) {
+    const int t = lane + 32 * r;
+    qn[r] = (t == 0) ? c1() : c0();  // q_E = 1
+    if (warp == 0 && t < NTL) Q[E * NTL + t] = qn[r];
+  }
+  team_sync<NW, TEAMS>(team);
+  for (int j = E - 1; j >= 0; --j) {
+    // partial m-sums of S_{j-1} (rows j+1 .. E are final)
+    double2 *pw = part + ((j & 1) * NW + warp) * NTL;
+#pragma unroll
+    for (int r = 0; r < NRT; ++r) {
+      const int t = lane + 32 * r;
+      double2 a0 = c0(), a1 = c0();
+      if (j >= 1 && t < NTL && t <= E - j + 1) {
+        const double2 *F = hb + (j - 1) * NTL + 1;  // F_{j-1}[m] = F[m]
+        const int mm = min(t - 1, E - j);
+        int m = 1 + warp;
+        const double2 *qd = Q + (j + m) * NTL + t - m - 1;  // q_{j+m}[t-m-1]
+        for (; m + NW <= mm; m += 2 * NW) {
+          a0 = cfma(F[m], qd[0], a0);
+          a1 = cfma(F[m + NW], qd[NW * (NTL - 1)], a1);
+          qd += 2 * NW * (NTL - 1);
+        }
+        if (m <= mm) a0 = cfma(F[m], qd[0], a0);
+      }
+      if (t < NTL) pw[t] = cadd(a0, a1);
+    }
+    if (warp == 0) {
+      // q_j = q_{j+1} - h_jj q_{j+1}[t-1] - S_j, S_j = sum of the partials written at j+1
+      const double2 h = hb[j * NTL + 1];
+      const double2 *pp = part + ((j + 1) & 1) * NW * NTL;
+      double2 last[NRT], up[NRT];
+#pragma unroll
+      for (int r = 0; r < NRT; ++r) last[r] = shfl2(qn[r], 31);
+#pragma unroll
+      for (int r = 0; r < NRT; ++r) {
+        const double2 s = shfl2(qn[r], (lane + 31) & 31);
+        up[r] = (lane != 0) ? s : (r == 0 ? c0() : last[r - 1]);
+      }
+#pragma unroll
+      for (int r = 0; r < NRT; ++r) {
+        const int t = lane + 32 * r;
+        double2 q = cfms(h, up[r], qn[r]);
+        if (j + 1 < E && t < NTL) {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) q = csub(q, pp[w * NTL + t]);
+        }
+        if (t > E - j) q = c0();  // above the degree of q_j
+        qn[r] = q;
+        if (t < NTL) Q[j * NTL + t] = q;
+      }
+    }
+    team_sync<NW, TEAMS>(team);
   }
 }
 
@@ -420,15 +484,23 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
   team_sync<NW, TEAMS>(team);
   LHAF_PHASE(2)
   double2 g = c0();
+  double2 *Q = T.u1;  // [E+1][NTL]: Q[j][t] = coefficient of x^{deg q_j - t}
+  {
+    double2 *part = Q + (E + 1) * NTL + 3 * (n + 2);  // [2][NW][NTL]
+    if constexpr (NW == 1) {
+      if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
+      else labudde<2>(hb, Q, E, NTL, lane);
+    } else {
+      if (NTL <= 32) labudde_team<1, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
+      else labudde_team<2, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
+    }
+  }
+  LHAF_PHASE(3)
   if (warp == 0) {
-    double2 *Q = T.u1;  // [E+1][NTL]: Q[j][t] = coefficient of x^{deg q_j - t}
-    if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
-    else labudde<2>(hb, Q, E, NTL, lane);
-    LHAF_PHASE(3)
     // ---- a8/a9: series from c_B = q_0, c_M = q_1 (loops) or c_M = q_0
     const double2 *cB = Q;
     const double2 *cM = loops ? Q + NTL : Q;
-    double2 *scr = Q + (E + 1) * NTL;
+    double2 *scr = Q + (E + 1) * NTL;  // series scratch (3 (n+2))
     if (n + 2 <= 32) g = series<1>(cM, cB, n, NTL, loops, scr, lane);
     else if (n + 2 <= 64) g = series<2>(cM, cB, n, NTL, loops, scr, lane);
     else g = series<5>(cM, cB, n, NTL, loops, scr, lane);
