@@ -345,21 +345,39 @@ __global__ void __launch_bounds__(128) prep_kernel(JobDev J) {
 }
 
 // ================================================================ finalize (a11-a12)
-__global__ void finalize_kernel(JobDev J, double2 *out, double *abs_out) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= J.npat) return;
+// One block per pattern: thread i double-double-sums the contiguous unit range
+// [i c, (i+1) c) in order, then thread 0 adds the 128 thread sums in order.  The order
+// depends only on the unit count, never on the rank count, so results are bit-identical for
+// any number of ranks.
+__global__ void __launch_bounds__(128) finalize_kernel(JobDev J, double2 *out, double *abs_out) {
+  __shared__ double s[128][6];
+  const int p = blockIdx.x;
   const PatDesc P = J.descs[p];
   if (P.d == 0) {  // N = 0
-    out[p] = make_double2(1.0, 0.0);
-    if (abs_out) abs_out[p] = 1.0;
+    if (threadIdx.x == 0) {
+      out[p] = make_double2(1.0, 0.0);
+      if (abs_out) abs_out[p] = 1.0;
+    }
     return;
   }
+  const uint64_t c = (P.units + 127) / 128;
+  const uint64_t ub = min(P.units, c * threadIdx.x), ue = min(P.units, ub + c);
   double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
-  for (uint64_t u = 0; u < P.units; ++u) {
+  for (uint64_t u = ub; u < ue; ++u) {
     const Partial q = J.partials[P.unit_begin + u];
     dd_add_dd(a0, a1, q.re_hi, q.re_lo);
     dd_add_dd(a2, a3, q.im_hi, q.im_lo);
     dd_add_dd(a4, a5, q.abs_hi, q.abs_lo);
+  }
+  s[threadIdx.x][0] = a0; s[threadIdx.x][1] = a1; s[threadIdx.x][2] = a2;
+  s[threadIdx.x][3] = a3; s[threadIdx.x][4] = a4; s[threadIdx.x][5] = a5;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  a0 = a1 = a2 = a3 = a4 = a5 = 0;
+  for (int i = 0; i < 128; ++i) {
+    dd_add_dd(a0, a1, s[i][0], s[i][1]);
+    dd_add_dd(a2, a3, s[i][2], s[i][3]);
+    dd_add_dd(a4, a5, s[i][4], s[i][5]);
   }
   const int e = 1 - P.n;  // 2^{1-n}: halving (x2) and the 2^{-n} prefactor, exact
   out[p] = make_double2(ldexp(a0 + a1, e), ldexp(a2 + a3, e));
@@ -406,7 +424,7 @@ cudaError_t launch_sieve(const JobDev &job, int variant, int dmax, int nmax, uin
 
 cudaError_t launch_finalize(const JobDev &job, double2 *out, double *abs_out, cudaStream_t s) {
   if (job.npat == 0) return cudaSuccess;
-  finalize_kernel<<<(job.npat + 127) / 128, 128, 0, s>>>(job, out, abs_out);
+  finalize_kernel<<<job.npat, 128, 0, s>>>(job, out, abs_out);
   return cudaGetLastError();
 }
 

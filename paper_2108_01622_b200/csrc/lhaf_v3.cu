@@ -63,6 +63,43 @@ __device__ __forceinline__ double2 rd_slot(const double2 (&A)[CS], int s) {
     if (i == s) v = A[i];
   return v;
 }
+// Switch-based (jump table) variants for the once-per-column compaction move.
+#define LHAF_CASES32(X)                                                                      \
+  X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15)      \
+  X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) \
+  X(31)
+template <int CS>
+__device__ __forceinline__ double2 rd_sw(const double2 (&A)[CS], int s) {
+  double2 v = c0();
+  switch (s) {
+#define LHAF_RD(i)                  \
+  case i:                           \
+    if constexpr (i < CS) v = A[i]; \
+    break;
+    LHAF_CASES32(LHAF_RD)
+#undef LHAF_RD
+    default: break;
+  }
+  return v;
+}
+template <int CS>
+__device__ __forceinline__ void wr_sw(double2 (&A)[CS], int s, double2 v) {
+  switch (s) {
+#define LHAF_WR(i)                  \
+  case i:                           \
+    if constexpr (i < CS) A[i] = v; \
+    break;
+    LHAF_CASES32(LHAF_WR)
+#undef LHAF_WR
+    default: break;
+  }
+}
+template <int S, int CS>
+__device__ __forceinline__ double2 read_pos(const double2 (&A)[CS], int q, int lane) {
+  double2 v = rd_sw<CS>(A, q / S);
+  if constexpr (S > 1) v = shfl2(v, (lane & ~(S - 1)) | (q & (S - 1)));
+  return v;
+}
 // value of column c (uniform) of this thread's row, on all S lanes of the row
 template <int S, int CS>
 __device__ __forceinline__ double2 read_col(const double2 (&A)[CS], int c, int lane) {
@@ -340,7 +377,8 @@ __device__ __forceinline__ double2 series(const double2 *cM, const double2 *cB, 
 
 // ================================================================ one term, one team
 // g(t) of one term (valid in warp 0 of the team); sign and weight from the decode (warp 0).
-template <int S, int CS, int NW, int TEAMS>
+// CMP: keep the live columns contiguous (compaction) and skip finished slot groups.
+template <int S, int CS, int NW, int TEAMS, bool CMP>
 __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J, uint64_t t,
                              const TeamMem &T, int tid, int team, int &sign, double &weight) {
   using Sh = Shape<S, CS, NW>;
@@ -384,10 +422,116 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
   double2 *kbuf = cand + 2 * NW * CC;                         // [2][RC]
   unsigned *keys = reinterpret_cast<unsigned *>(kbuf + 2 * RC);  // [2][NW][4] (key, phys)
   int label = rr;
-  uint64_t live = (E >= 64 ? ~0ull : ((1ull << E) - 1ull)) & ~1ull;  // indices with label > k
   double2 colv = (S == 1) ? A[0] : shfl2(A[0], lane & ~(S - 1));    // this row's B[.][k]
   int buf = 0;
   const int kend = E >= 2 ? E - 2 : 0;
+  if constexpr (CMP) {
+    // live column positions are [lo, E); the lowest live column moves into the position the
+    // pivot column frees; slot groups of 4 below lo are skipped with a uniform branch
+    constexpr int NG = (CS + 3) / 4;
+    int lo = 1;
+    int mypos = rr;  // position of this index's column while it is live, else -1
+    for (int k = 0; k < kend; ++k) {
+      double2 *cb = cand + buf * NW * CC;
+      double2 *kb = kbuf + buf * RC;
+      unsigned *yk = keys + buf * NW * 4;
+      double2 *yv = reinterpret_cast<double2 *>(keys + 2 * NW * 4) + buf * NW;
+      buf ^= 1;
+      const int glo = lo / (4 * S);
+      const bool candr = label > k && label < E;
+      unsigned key = 0u;
+      if (candr) {
+        const unsigned fbits = __float_as_uint((float)(fabs(colv.x) + fabs(colv.y)));
+        key = (((fbits >> 6) + 1u) << 6) | (unsigned)(63 - label);
+      }
+      const unsigned wkey = __reduce_max_sync(LHAF_FULL, key);
+      if (par == 0 && mypos >= 0) kb[mypos] = candr ? colv : c0();
+      if (tid < lo - 4 * S * glo) kb[4 * S * glo + tid] = c0();  // dead head of the first group
+      if (candr && key == wkey) {
+        double2 *dst = cb + warp * CC + par;
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+          if (g >= glo) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (4 * g + i < CS) dst[S * (4 * g + i)] = A[4 * g + i];
+          }
+        if (par == 0) {
+          yv[warp] = colv;
+          yk[4 * warp + 1] = (unsigned)rr;
+          yk[4 * warp + 2] = (unsigned)mypos;
+        }
+      }
+      if (lane == 0) yk[4 * warp] = wkey;
+      team_sync<NW, TEAMS>(team);
+
+      unsigned bkey = 0u;
+      int wb = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const unsigned kw = yk[4 * w];
+        if (kw > bkey) { bkey = kw; wb = w; }
+      }
+      const int plabel = 63 - (int)(bkey & 63u);
+      const int p = (int)yk[4 * wb + 1];
+      const int qp = (int)yk[4 * wb + 2];  // column position of the pivot index
+      const int newlabel = (rr == p) ? k + 1 : (label == k + 1 ? plabel : label);
+      if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL) hb[newlabel * NTL + k + 1 - newlabel] = colv;
+      if ((bkey >> 6) > 1u) {
+        const double2 piv = yv[wb];
+        const double2 ip = crecip(piv);
+        const double2 m = (candr && rr != p) ? cmul(colv, ip) : c0();
+        const double2 *rp = cb + wb * CC + par;
+        const double2 *kq = kb + par;
+        double xr0 = 0, xi0 = 0, yr0 = 0, yi0 = 0, xr1 = 0, xi1 = 0, yr1 = 0, yi1 = 0;
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+          if (g >= glo) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int s = 4 * g + i;
+              if (s < CS) {
+                const double2 r = rp[S * s];
+                const double2 q = kq[S * s];
+                double2 a = cfms(m, r, A[s]);
+                A[s] = a;
+                if (s & 1) {
+                  xr1 = fma(a.x, q.x, xr1); xi1 = fma(a.y, q.y, xi1);
+                  yr1 = fma(a.x, q.y, yr1); yi1 = fma(a.y, q.x, yi1);
+                } else {
+                  xr0 = fma(a.x, q.x, xr0); xi0 = fma(a.y, q.y, xi0);
+                  yr0 = fma(a.x, q.y, yr0); yi0 = fma(a.y, q.x, yi0);
+                }
+              }
+            }
+          }
+        double2 sum = make_double2((xr0 + xr1) - (xi0 + xi1), (yr0 + yr1) + (yi0 + yi1));
+#pragma unroll
+        for (int x = 1; x < S; x <<= 1) sum = cadd(sum, shfl2_xor(sum, x));
+        colv = cmul(sum, ip);
+      } else {
+        colv = read_pos<S, CS>(A, qp, lane);  // nothing to eliminate: column p as it stands
+      }
+      // compaction: the column at position lo moves into the pivot column's position
+      if (qp != lo) {
+        const double2 x = read_pos<S, CS>(A, lo, lane);
+        if (par == qp % S) wr_sw<CS>(A, qp / S, x);
+        if (mypos == lo) mypos = qp;
+      }
+      if (rr == p) mypos = -1;
+      lo += 1;
+      label = newlabel;
+    }
+    // the last two columns: the carried one (label kend) and the last live one (position lo)
+    if (E >= 1) {
+      if (par == 0 && label < E && kend + 1 - label < NTL) hb[label * NTL + kend + 1 - label] = colv;
+      if (E >= 2) {
+        const double2 cl = read_pos<S, CS>(A, lo, lane);
+        if (par == 0 && label < E && E - label < NTL) hb[label * NTL + E - label] = cl;
+      }
+    }
+  } else {
+  uint64_t live = (E >= 64 ? ~0ull : ((1ull << E) - 1ull)) & ~1ull;  // indices with label > k
   for (int k = 0; k < kend; ++k) {
     double2 *cb = cand + buf * NW * CC;
     double2 *kb = kbuf + buf * RC;
@@ -414,7 +558,9 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
       }
     }
     if (lane == 0) yk[4 * warp] = wkey;
+    LHAF_PHASE(6)
     team_sync<NW, TEAMS>(team);
+    LHAF_PHASE(7)
 
     unsigned bkey = 0u;
     int wb = 0;
@@ -459,6 +605,7 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
       colv = read_col<S, CS>(A, p, lane);  // nothing to eliminate: column p as it stands
     }
     label = newlabel;
+    LHAF_PHASE(1)
   }
   // the last two columns: the carried one (label kend) and the remaining live index
   if (E >= 1) {
@@ -468,6 +615,7 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
       const double2 cl = read_col<S, CS>(A, pl, lane);
       if (par == 0 && label < E && E - label < NTL) hb[label * NTL + E - label] = cl;
     }
+  }
   }
   team_sync<NW, TEAMS>(team);
   LHAF_PHASE(1)
@@ -512,7 +660,7 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
 }
 
 // ================================================================ kernels
-template <int S, int CS, int NW, int TEAMS, int REGS>
+template <int S, int CS, int NW, int TEAMS, int REGS, bool CMP>
 __global__ void __maxnreg__(REGS)
 sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
   extern __shared__ double2 smem[];
@@ -537,7 +685,7 @@ sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
     for (uint64_t t = tb + team; t < te; t += TEAMS) {
       int sign = 1;
       double weight = 1.0;
-      const double2 g = team_term<S, CS, NW, TEAMS>(P, D, J, t, T, tid, team, sign, weight);
+      const double2 g = team_term<S, CS, NW, TEAMS, CMP>(P, D, J, t, T, tid, team, sign, weight);
       if (tid == 0) {
         const double sw = sign * weight;
         dd_add(rh, rl, sw * g.x);
@@ -566,7 +714,7 @@ sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
 }
 
 // g(t) (unweighted) of pattern 0 for a list of term indices; one team per index.
-template <int S, int CS, int NW, int TEAMS, int REGS>
+template <int S, int CS, int NW, int TEAMS, int REGS, bool CMP>
 __global__ void __maxnreg__(REGS)
 terms_v3(JobDev J, const uint64_t *ts, int nt, double2 *g_out, int team_words) {
   extern __shared__ double2 smem[];
@@ -583,14 +731,14 @@ terms_v3(JobDev J, const uint64_t *ts, int nt, double2 *g_out, int team_words) {
     if (i < nt) {
       int sign;
       double weight;
-      const double2 g = team_term<S, CS, NW, TEAMS>(P, D, J, ts[i], T, tid, team, sign, weight);
+      const double2 g = team_term<S, CS, NW, TEAMS, CMP>(P, D, J, ts[i], T, tid, team, sign, weight);
       if (tid == 0) g_out[i] = g;
     }
   }
 }
 
 // ================================================================ host side
-template <int S, int CS, int NW, int TEAMS, int REGS>
+template <int S, int CS, int NW, int TEAMS, int REGS, bool CMP = false>
 struct Inst {
   using Sh = Shape<S, CS, NW>;
   static constexpr int EMAX = Sh::EMAX;
@@ -599,7 +747,7 @@ struct Inst {
                            int num_sms, cudaStream_t s) {
     const int tw = Sh::words(E, NTL, n);
     const size_t smem = (size_t)tw * TEAMS * sizeof(double2);
-    auto *kern = sieve_v3<S, CS, NW, TEAMS, REGS>;
+    auto *kern = sieve_v3<S, CS, NW, TEAMS, REGS, CMP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -620,7 +768,7 @@ struct Inst {
                            double2 *g_out, cudaStream_t s) {
     const int tw = Sh::words(E, NTL, n);
     const size_t smem = (size_t)tw * TEAMS * sizeof(double2);
-    auto *kern = terms_v3<S, CS, NW, TEAMS, REGS>;
+    auto *kern = terms_v3<S, CS, NW, TEAMS, REGS, CMP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int grid = (nt + TEAMS - 1) / TEAMS;
@@ -644,6 +792,9 @@ using A26 = Inst<2, 13, 2, 2, 104>;   // E <= 26: 4 warps / CTA
 using A48 = Inst<4, 12, 6, 1, 104>;   // E <= 48: 6 warps / CTA
 using A64 = Inst<4, 16, 8, 1, 128>;   // E <= 64: 8 warps / CTA
 using B62 = Inst<2, 31, 4, 1, 200>;   // (LHAF_V3_ALT=2) E <= 62 without spills: 2 CTAs / SM
+using C25 = Inst<1, 25, 1, 4, 168, true>;  // (LHAF_V3_ALT=3) compaction variants
+using C48 = Inst<2, 24, 3, 1, 168, true>;
+using C62 = Inst<2, 31, 4, 1, 200, true>;
 static int alt_mode() {
   static const int m = [] { const char *e = getenv("LHAF_V3_ALT"); return e ? atoi(e) : 0; }();
   return m;
@@ -674,6 +825,11 @@ extern "C" int lhaf_debug_phase_cycles(unsigned long long *out8) {
 
 #define LHAF_V3_DISPATCH(CALL)                  \
   if (v3::alt_mode() == 2 && E > 48 && E <= v3::B62::EMAX) return v3::B62::CALL; \
+  if (v3::alt_mode() == 3) {                    \
+    if (E > 17 && E <= v3::C25::EMAX) return v3::C25::CALL; \
+    if (E > 32 && E <= v3::C48::EMAX) return v3::C48::CALL; \
+    if (E > 48 && E <= v3::C62::EMAX) return v3::C62::CALL; \
+  }                                             \
   if (v3::alt_mode() == 1) {                    \
     if (E <= v3::A26::EMAX && E > 17) return v3::A26::CALL; \
     if (E <= v3::A48::EMAX && E > 32) return v3::A48::CALL; \

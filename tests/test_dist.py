@@ -34,17 +34,28 @@ def two_sum(a, b):
     return s, (a - (s - bb)) + (b - bb)
 
 
+def _dd_add(acc, hi2, lo2):
+    s, e = two_sum(acc[0], hi2)
+    e += acc[1] + lo2
+    hi = s + e
+    return [hi, e - (hi - s)]
+
+
 def dd_finalize(P):
-    """Python mirror of the finalize order: dd-sum units in ascending order."""
+    """Python mirror of finalize_kernel's fixed order: 128 contiguous unit ranges are each
+    double-double summed in ascending order, then the 128 range sums in ascending order
+    (the order depends only on the unit count, not on the number of ranks)."""
+    units = P.shape[0]
+    c = (units + 127) // 128
     out = []
-    for c in (0, 2):
-        hi = lo = 0.0
-        for u in range(P.shape[0]):
-            s, e = two_sum(hi, P[u, c])
-            e += lo + P[u, c + 1]
-            hi = s + e
-            lo = e - (hi - s)
-        out.append(hi + lo)
+    for col in (0, 2):
+        total = [0.0, 0.0]
+        for i in range(128):
+            acc = [0.0, 0.0]
+            for u in range(min(units, c * i), min(units, c * i + c)):
+                acc = _dd_add(acc, P[u, col], P[u, col + 1])
+            total = _dd_add(total, acc[0], acc[1])
+        out.append(total[0] + total[1])
     return out
 
 

@@ -197,3 +197,98 @@ def test_errors(lib):
     with pytest.raises(lib.LhafError) as e:
         lib.lhaf_rpt(np.eye(130), np.ones(130), np.ones(130, np.int32))   # d = 130 > 64
     assert e.value.status == 3
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3])
+def test_kernel_variants_agree_with_oracle(lib, orc, variant):
+    # every kernel variant (v1 Householder baseline, v2 aux-warp, v3 default) on loop and
+    # loop-free patterns with collisions, odd N (phantom) and a mixed-state pattern
+    rng = G.rng_for(4242)
+    k = 7
+    A = G.pure_B(G.haar_unitary(k, rng), 0.85)
+    g = G.complex_gaussian(k, 0.4, rng)
+    cases = [([2, 1, 0, 3, 1, 0, 2], g), ([1, 1, 1, 1, 1, 1, 1], g), ([3, 0, 2, 0, 0, 1, 1], np.zeros(k)),
+             ([0, 4, 0, 0, 0, 0, 1], g)]
+    lib.lhaf_set_kernel(variant)
+    try:
+        for reps, gg in cases:
+            ref = orc.lhaf(A, gg, reps)
+            got = lib.lhaf_rpt(A, gg, reps)
+            if abs(ref) == 0.0:   # odd N without loops: exactly 0, rounding-level output
+                assert abs(got) <= 1e-14, (variant, reps, got)
+            else:
+                assert rel(got, ref) <= 1e-10, (variant, reps, got, ref)
+        U = G.haar_unitary(4, rng)
+        A2 = G.lossy_squeezed_A2(U, 0.6, 0.7)
+        g2 = G.complex_gaussian(8, 0.2, rng)
+        ref = orc.lhaf_mixed(A2, g2, [2, 1, 0, 2])
+        assert rel(lib.lhaf_rpt_mixed(A2, g2, [2, 1, 0, 2]), ref) <= 1e-10
+    finally:
+        lib.lhaf_set_kernel(0)
+
+
+def test_batch_mixing_dims_and_loop_flags(lib, orc):
+    # one job whose patterns span reduced dimensions 2..44 and both loop flags: the kernel is
+    # instantiated for the largest bordered size and every smaller pattern runs padded
+    rng = G.rng_for(777)
+    k = 24
+    A = G.pure_B(G.haar_unitary(k, rng), 0.8)
+    gam = np.stack([G.complex_gaussian(k, 0.3, rng) for _ in range(6)])
+    gam[1] = 0.0
+    gam[4] = 0.0
+    pats = np.zeros((6, k), np.int32)
+    pats[0, :2] = 1                      # d = 2
+    pats[1, :6] = [2, 2, 1, 1, 0, 2]     # no loops, collisions
+    pats[2, :10] = 1                     # d = 10
+    pats[3, :5] = [3, 1, 1, 2, 1]
+    pats[4, :16] = 1                     # no loops, d = 16
+    pats[5, :22] = 1                     # d = 22 (+1 border)
+    got = lib.lhaf_rpt_batch(A, gam, pats, gamma_per_pattern=True)
+    for b in range(6):
+        ref = orc.lhaf(A, gam[b], pats[b])
+        assert rel(got[b], ref) <= 1e-10, (b, got[b], ref)
+
+
+def test_block_diagonal_N40(lib, orc):
+    # Fig. 5 protocol at N = 40 through the full sieve (2^19 evaluated terms, d = 40):
+    # lhaf(A1 (+) A2) = lhaf(A1) lhaf(A2), rows/cols permuted so pairs straddle the blocks
+    rng = G.rng_for(510)
+    m = 20
+    A1 = G.random_symmetric(m, rng, 0.5)
+    A2 = G.random_symmetric(m, rng, 0.5)
+    g1 = G.complex_gaussian(m, 0.5, rng)
+    g2 = G.complex_gaussian(m, 0.5, rng)
+    Z = np.zeros((m, m), complex)
+    A = np.block([[A1, Z], [Z, A2]])
+    g = np.concatenate([g1, g2])
+    perm = rng.permutation(2 * m)
+    Ap = A[np.ix_(perm, perm)]
+    gp = g[perm]
+    one = np.ones(m, np.int32)
+    want = orc.lhaf(A1, g1, one, method="et") * orc.lhaf(A2, g2, one, method="et")
+    got = lib.lhaf_rpt(Ap, gp, np.ones(2 * m, np.int32))
+    assert rel(got, want) <= 1e-8, (got, want)
+
+
+def test_pure_mixed_factorisation_full_size(lib):
+    # P:104-107 / P:332 at config-5 scale (pure limit eta = 1, m = 100): lhaf_mixed(B (+) B*)
+    # over the doubled pattern equals |lhaf(B, 0, n)|^2.  In the pure limit the natural pairs
+    # (i, i+k) have zero coupling, so the mixed sieve cancels strongly (kappa = sum|term| /
+    # |lhaf| = 6e5 and 5e7 for the two patterns, the same in the oracle); the bound is 1e-8
+    # where kappa allows it and the a-priori FP64 bound 64 kappa eps otherwise.
+    for mult in ([2, 1, 2, 1, 2, 1, 2, 1, 1, 1], [3, 2, 3, 1, 2, 2, 3, 2]):
+        rng = G.rng_for(1005)
+        U = G.haar_unitary(100, rng)
+        A2 = G.lossy_squeezed_A2(U, 0.9, 1.0)
+        B = G.pure_B(U, 0.9)
+        reps = np.zeros(100, np.int32)
+        reps[rng.choice(100, len(mult), replace=False)] = mult
+        job = lib.Job(A2, np.zeros(200), reps, mixed=True)
+        job.reset(); job.run()
+        mixed = job.finalize()[0]
+        kappa = job.abs_sum()[0] / abs(mixed)
+        job.close()
+        pure = lib.lhaf_rpt(B, np.zeros(100), reps)
+        assert rel(mixed, abs(pure) ** 2) <= max(1e-8, 64 * kappa * 2.0 ** -53), (mult, mixed, abs(pure) ** 2, kappa)
+        if kappa < 1e6:
+            assert rel(mixed, abs(pure) ** 2) <= 1e-8

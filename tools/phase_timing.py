@@ -26,8 +26,9 @@ for c in [int(x) for x in sys.argv[2:]] or [2, 4, 5]:
     job.reset(); job.run(0, U); torch.cuda.synchronize()
     lib.lhaf_debug_phase_cycles(buf)
     terms = job.terms * U / job.units
-    names = ["decode+build", "reduction", "band->F", "La Budde", "series", "end barrier"]
-    tot = sum(buf[i] for i in range(6))
+    names = ["decode+build", "column: update+carry", "band->F", "La Budde", "series", "end barrier",
+             "column: pivot+publish", "column: barrier wait"]
+    tot = sum(buf[i] for i in range(8))
     print(f"cfg{c}: terms={terms:.0f} cycles/term (thread 0 of each team): " +
           ", ".join(f"{nm}={buf[i]/terms:.0f} ({100*buf[i]/tot:.0f}%)" for i, nm in enumerate(names)), flush=True)
     job.close()
