@@ -135,7 +135,7 @@ template <int S, int CS, int NW>
 struct Shape {
   static constexpr int TS = 32 * NW, RC = TS / S, CC = S * CS;
   static constexpr int EMAX = RC < CC ? RC : CC;
-  __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 4 * NW; }
+  __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 6 * NW; }
   __host__ __device__ static int u1_words(int E, int NTL, int n) {
     const int lab = (E + 1) * NTL + 3 * (n + 2) + 2 * NW * NTL;
     return red_words() > lab ? red_words() : lab;
@@ -536,7 +536,7 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
     double2 *cb = cand + buf * NW * CC;
     double2 *kb = kbuf + buf * RC;
     unsigned *yk = keys + buf * NW * 4;
-    double2 *yv = reinterpret_cast<double2 *>(keys + 2 * NW * 4) + buf * NW;  // pivot values
+    double2 *yv = reinterpret_cast<double2 *>(keys + 2 * NW * 4) + buf * NW * 2;  // pivot, 1/pivot
     buf ^= 1;
     const bool candr = label > k && label < E;
     // pivot key: |re| + |im| as a float (monotone bits), low 6 bits = 63 - label so that ties
@@ -548,12 +548,13 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
     }
     const unsigned wkey = __reduce_max_sync(LHAF_FULL, key);
     if (par == 0) kb[rr] = candr ? colv : c0();
-    if (candr && key == wkey) {  // this warp's best row publishes itself
+    if (candr && key == wkey) {  // this warp's best row publishes itself (and 1 / its pivot)
       double2 *dst = cb + warp * CC + par;
 #pragma unroll
       for (int s = 0; s < CS; ++s) dst[S * s] = A[s];
       if (par == 0) {
-        yv[warp] = colv;
+        yv[2 * warp] = colv;
+        if constexpr (NW > 1) yv[2 * warp + 1] = crecip(colv);  // off the post-barrier path
         yk[4 * warp + 1] = (unsigned)rr;
       }
     }
@@ -576,8 +577,7 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
     if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL) hb[newlabel * NTL + k + 1 - newlabel] = colv;
     live &= ~(1ull << p);
     if ((bkey >> 6) > 1u) {  // nonzero pivot
-      const double2 piv = yv[wb];
-      const double2 ip = crecip(piv);
+      const double2 ip = (NW > 1) ? yv[2 * wb + 1] : crecip(yv[2 * wb]);
       const double2 m = (candr && rr != p) ? cmul(colv, ip) : c0();
       const double2 *rp = cb + wb * CC + par;
       const double2 *kq = kb + par;
@@ -785,16 +785,17 @@ using I17 = Inst<1, 17, 1, 4, 128>;
 using I25 = Inst<1, 25, 1, 4, 168>;
 using I32 = Inst<1, 32, 1, 4, 168>;
 using I48 = Inst<2, 24, 3, 1, 168>;
-using I62 = Inst<2, 31, 4, 1, 200>;  // 2 CTAs / SM, no spills
+using D48 = Inst<2, 24, 3, 1, 255>;  // (LHAF_V3_ALT=4)
+using I62 = Inst<2, 31, 4, 1, 255>;  // 2 CTAs / SM (2 warps per 16K-register sub-partition)
 using I64 = Inst<2, 32, 4, 1, 168>;
 // alternatives (LHAF_V3_ALT=1): more lanes per row, fewer registers, more warps per SM
 using A26 = Inst<2, 13, 2, 2, 104>;   // E <= 26: 4 warps / CTA
 using A48 = Inst<4, 12, 6, 1, 104>;   // E <= 48: 6 warps / CTA
 using A64 = Inst<4, 16, 8, 1, 128>;   // E <= 64: 8 warps / CTA
-using B62 = Inst<2, 31, 4, 1, 200>;   // (LHAF_V3_ALT=2) E <= 62 without spills: 2 CTAs / SM
+using B62 = Inst<2, 31, 4, 1, 232>;   // (LHAF_V3_ALT=2) E <= 62, 232 registers
 using C25 = Inst<1, 25, 1, 4, 168, true>;  // (LHAF_V3_ALT=3) compaction variants
 using C48 = Inst<2, 24, 3, 1, 168, true>;
-using C62 = Inst<2, 31, 4, 1, 200, true>;
+using C62 = Inst<2, 31, 4, 1, 232, true>;
 static int alt_mode() {
   static const int m = [] { const char *e = getenv("LHAF_V3_ALT"); return e ? atoi(e) : 0; }();
   return m;
@@ -825,6 +826,7 @@ extern "C" int lhaf_debug_phase_cycles(unsigned long long *out8) {
 
 #define LHAF_V3_DISPATCH(CALL)                  \
   if (v3::alt_mode() == 2 && E > 48 && E <= v3::B62::EMAX) return v3::B62::CALL; \
+  if (v3::alt_mode() == 4 && E > 32 && E <= v3::D48::EMAX) return v3::D48::CALL; \
   if (v3::alt_mode() == 3) {                    \
     if (E > 17 && E <= v3::C25::EMAX) return v3::C25::CALL; \
     if (E > 32 && E <= v3::C48::EMAX) return v3::C48::CALL; \
