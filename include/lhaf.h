@@ -108,6 +108,18 @@ lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_s
 lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t *reps,
                            int32_t k, double out[2]);
 
+/* Cutoff-batched loop hafnians for the chain rule (App. B.5, P:517-523:
+ * "all but one mode has a fixed outcome n_fixed, while one 'batched' mode takes all values
+ * from 0 to the cutoff n_cut").  out[2 j], out[2 j + 1] = lhaf(A_n) for the pattern
+ * reps_fixed with reps[mode] replaced by j, j = 0 .. n_cut.  A: k*k c128, gamma: k c128,
+ * reps_fixed: k int32 (its entry at `mode` is ignored), 0 <= mode < k, 0 <= n_cut <= 64,
+ * out: 2 (n_cut + 1) doubles.  All n_cut + 1 patterns are evaluated in ONE device job (one
+ * sieve launch over their work units); the paper's further saving — one cubic step shared by
+ * all counts of the batched mode — is not implemented yet (the per-count sieves are
+ * independent).  Errors as lhaf_rpt_batch, plus LHAF_E_ARG for a bad mode / n_cut. */
+lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
+                            int32_t k, int32_t mode, int32_t n_cut, double *out);
+
 /* Same three entry points with DEVICE pointers for A / gamma / out (reps stays on the host,
  * since planning is host integer work) and an explicit cudaStream_t (passed as void*; NULL =
  * the legacy default stream).  The call is asynchronous with respect to the host only in the

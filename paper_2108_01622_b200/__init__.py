@@ -67,6 +67,7 @@ def _load() -> ctypes.CDLL:
         "lhaf_rpt": ([dp, dp, ip, ctypes.c_int32, dp]),
         "lhaf_rpt_batch": ([dp, dp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32, dp]),
         "lhaf_rpt_mixed": ([dp, dp, ip, ctypes.c_int32, dp]),
+        "lhaf_rpt_cutoff": ([dp, dp, ip, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, dp]),
         "lhaf_rpt_batch_dev": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
                                 ctypes.c_int32, vp, vp]),
         "lhaf_job_create": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
@@ -123,7 +124,7 @@ def reload_library():
     return _lib
 
 # every symbol include/lhaf.h declares (checked by tests/test_capi.py)
-EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed",
+EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed", "lhaf_rpt_cutoff",
             "lhaf_rpt_batch_dev", "lhaf_job_create", "lhaf_job_info_get", "lhaf_job_reset",
             "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_finalize", "lhaf_job_abs_sum",
             "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
@@ -195,6 +196,14 @@ def lhaf_rpt_mixed(A2, gamma2, reps) -> complex:
     out = np.zeros(2)
     _check(_lib.lhaf_rpt_mixed(_dp(A2), _dp(gamma2), _ip(reps), reps.shape[0], _dp(out)))
     return complex(out[0], out[1])
+
+
+def lhaf_rpt_cutoff(A, gamma, reps_fixed, mode: int, n_cut: int) -> np.ndarray:
+    """lhaf for the pattern reps_fixed with reps[mode] = 0 .. n_cut (App. B.5), one job."""
+    A, gamma, reps = _c128(A), _c128(gamma), _i32(reps_fixed)
+    out = np.zeros(2 * (n_cut + 1))
+    _check(_lib.lhaf_rpt_cutoff(_dp(A), _dp(gamma), _ip(reps), reps.shape[0], mode, n_cut, _dp(out)))
+    return out[0::2] + 1j * out[1::2]
 
 
 def lhaf_rpt_batch_dev(A_dev_ptr: int, gamma_dev_ptr: int, gamma_stride: int, reps_batch,

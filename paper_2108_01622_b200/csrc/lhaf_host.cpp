@@ -605,6 +605,20 @@ lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_s
   return s;
 }
 
+lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
+                            int32_t k, int32_t mode, int32_t n_cut, double *out) {
+  if (!A || !gamma || !reps_fixed || !out) return fail(LHAF_E_ARG, "null pointer argument");
+  if (k < 1 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "k = %d out of range", k);
+  if (mode < 0 || mode >= k) return fail(LHAF_E_ARG, "batched mode %d outside [0, %d)", mode, k);
+  if (n_cut < 0 || n_cut > 64) return fail(LHAF_E_ARG, "n_cut = %d outside [0, 64]", n_cut);
+  std::vector<int32_t> reps((size_t)(n_cut + 1) * k);
+  for (int j = 0; j <= n_cut; ++j) {
+    memcpy(&reps[(size_t)j * k], reps_fixed, (size_t)k * sizeof(int32_t));
+    reps[(size_t)j * k + mode] = j;
+  }
+  return lhaf_rpt_batch(A, gamma, 0, reps.data(), k, n_cut + 1, out);
+}
+
 lhaf_status lhaf_rpt(const double *A, const double *gamma, const int32_t *reps, int32_t k,
                      double out[2]) {
   return lhaf_rpt_batch(A, gamma, 0, reps, k, 1, out);

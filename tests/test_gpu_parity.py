@@ -292,3 +292,24 @@ def test_pure_mixed_factorisation_full_size(lib):
         assert rel(mixed, abs(pure) ** 2) <= max(1e-8, 64 * kappa * 2.0 ** -53), (mult, mixed, abs(pure) ** 2, kappa)
         if kappa < 1e6:
             assert rel(mixed, abs(pure) ** 2) <= 1e-8
+
+
+def test_cutoff_batched_chain_rule(lib, orc):
+    # App. B.5: one mode takes 0..n_cut with the others fixed; every value equals
+    # the individually computed lhaf (oracle), including odd counts (phantom) and n = 0
+    rng = G.rng_for(523)
+    k = 8
+    A = G.pure_B(G.haar_unitary(k, rng), 0.8)
+    g = G.complex_gaussian(k, 0.3, rng)
+    fixed = np.array([1, 2, 0, 1, 0, 1, 0, 0], np.int32)
+    vals = lib.lhaf_rpt_cutoff(A, g, fixed, 2, 8)
+    assert vals.shape == (9,)
+    for j in range(9):
+        reps = fixed.copy()
+        reps[2] = j
+        ref = orc.lhaf(A, g, reps)
+        assert rel(vals[j], ref) <= 1e-10, (j, vals[j], ref)
+    # n_cut = 0 equals the plain call; bad arguments are rejected
+    assert rel(lib.lhaf_rpt_cutoff(A, g, fixed, 2, 0)[0], lib.lhaf_rpt(A, g, fixed)) <= 1e-15
+    with pytest.raises(lib.LhafError):
+        lib.lhaf_rpt_cutoff(A, g, fixed, k, 3)
