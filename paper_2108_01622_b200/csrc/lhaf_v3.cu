@@ -138,7 +138,9 @@ struct Shape {
   __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 6 * NW; }
   __host__ __device__ static int u1_words(int E, int NTL, int n) {
     const int lab = (E + 1) * NTL + 3 * (n + 2) + 2 * NW * NTL;
-    return red_words() > lab ? red_words() : lab;
+    const int cmp = RC * S * ((3 * CS + 3) / 4);  // phased reduction buffer
+    int w = red_words() > lab ? red_words() : lab;
+    return w > cmp ? w : cmp;
   }
   __host__ __device__ static int words(int E, int NTL, int n) {
     return E * NTL + u1_words(E, NTL, n) + 32 + 32;
@@ -375,6 +377,185 @@ __device__ __forceinline__ double2 series(const double2 *cM, const double2 *cB, 
   return warp_sum2(gp);
 }
 
+// ================================================================ phased reduction
+// The Hessenberg reduction in four phases of shrinking register arrays.  Live columns (index
+// label > k) occupy "positions" (slot S*s + par); at the start of phases 2..4 the live
+// columns of every row are compacted (through shared memory, one row per S lanes) to the
+// positions 0..L-1 (ascending index order), so later phases sweep CS2 = 3CS/4, CS3 = CS/2,
+// CS4 = CS/4 slots instead of CS.  kb and the published pivot rows are indexed by position.
+struct PhaseSt {
+  int label, buf, mypos;
+  uint64_t live, livec;  // indices with label > k; the live set at the last compaction
+  double2 colv;
+};
+
+template <int S, int CS, int CSP, int NW, int TEAMS>
+__device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int k0, int k1, int E,
+                                            int NTL, double2 *hb, double2 *u1, int tid, int team) {
+  using Sh = Shape<S, CS, NW>;
+  constexpr int RC = Sh::RC, CC = Sh::CC;
+  const int lane = tid & 31, warp = tid >> 5, rr = tid / S, par = tid % S;
+  double2 *cand = u1;                                             // [2][NW][CC]
+  double2 *kbuf = cand + 2 * NW * CC;                             // [2][RC]
+  unsigned *keys = reinterpret_cast<unsigned *>(kbuf + 2 * RC);   // [2][NW][4]
+  for (int k = k0; k < k1; ++k) {
+    double2 *cb = cand + st.buf * NW * CC;
+    double2 *kb = kbuf + st.buf * RC;
+    unsigned *yk = keys + st.buf * NW * 4;
+    double2 *yv = reinterpret_cast<double2 *>(keys + 2 * NW * 4) + st.buf * NW * 2;
+    st.buf ^= 1;
+    const bool candr = st.label > k && st.label < E;
+    unsigned key = 0u;
+    if (candr) {
+      const unsigned fbits = __float_as_uint((float)(fabs(st.colv.x) + fabs(st.colv.y)));
+      key = (((fbits >> 6) + 1u) << 6) | (unsigned)(63 - st.label);
+    }
+    const unsigned wkey = __reduce_max_sync(LHAF_FULL, key);
+    if (par == 0 && st.mypos >= 0) kb[st.mypos] = candr ? st.colv : c0();
+    if (candr && key == wkey) {  // this warp's best row publishes itself (and 1 / its pivot)
+      double2 *dst = cb + warp * CC + par;
+#pragma unroll
+      for (int s = 0; s < CSP; ++s) dst[S * s] = A[s];
+      if (par == 0) {
+        yv[2 * warp] = st.colv;
+        if constexpr (NW > 1) yv[2 * warp + 1] = crecip(st.colv);
+        yk[4 * warp + 1] = (unsigned)rr;
+        yk[4 * warp + 2] = (unsigned)st.mypos;
+      }
+    }
+    if (lane == 0) yk[4 * warp] = wkey;
+    team_sync<NW, TEAMS>(team);
+
+    unsigned bkey = 0u;
+    int wb = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const unsigned kw = yk[4 * w];
+      if (kw > bkey) { bkey = kw; wb = w; }
+    }
+    const int plabel = 63 - (int)(bkey & 63u);
+    const int p = (int)yk[4 * wb + 1];   // pivot: physical index
+    const int qp = (int)yk[4 * wb + 2];  // and its column position
+    const int newlabel = (rr == p) ? k + 1 : (st.label == k + 1 ? plabel : st.label);
+    if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL) hb[newlabel * NTL + k + 1 - newlabel] = st.colv;
+    st.live &= ~(1ull << p);
+    if ((bkey >> 6) > 1u) {
+      const double2 ip = (NW > 1) ? yv[2 * wb + 1] : crecip(yv[2 * wb]);
+      const double2 m = (candr && rr != p) ? cmul(st.colv, ip) : c0();
+      const double2 *rp = cb + wb * CC + par;
+      const double2 *kq = kb + par;
+      double xr0 = 0, xi0 = 0, yr0 = 0, yi0 = 0, xr1 = 0, xi1 = 0, yr1 = 0, yi1 = 0;
+#pragma unroll
+      for (int s = 0; s < CSP; ++s) {
+        const double2 r = rp[S * s];
+        const double2 q = kq[S * s];
+        double2 a = cfms(m, r, A[s]);
+        A[s] = a;
+        if (s & 1) {
+          xr1 = fma(a.x, q.x, xr1); xi1 = fma(a.y, q.y, xi1);
+          yr1 = fma(a.x, q.y, yr1); yi1 = fma(a.y, q.x, yi1);
+        } else {
+          xr0 = fma(a.x, q.x, xr0); xi0 = fma(a.y, q.y, xi0);
+          yr0 = fma(a.x, q.y, yr0); yi0 = fma(a.y, q.x, yi0);
+        }
+      }
+      double2 sum = make_double2((xr0 + xr1) - (xi0 + xi1), (yr0 + yr1) + (yi0 + yi1));
+#pragma unroll
+      for (int x = 1; x < S; x <<= 1) sum = cadd(sum, shfl2_xor(sum, x));
+      st.colv = cmul(sum, ip);
+    } else {
+      st.colv = read_col<S, CSP>(A, qp, lane);  // nothing to eliminate: column p as it stands
+    }
+    st.label = newlabel;
+  }
+}
+
+// Compaction of every row's live columns from CSA to CSB slots (see above).  ipos[q] = index
+// of the column at position q (-1: none).
+template <int S, int CS, int CSA, int CSB, int NW, int TEAMS>
+__device__ __forceinline__ void compact(const double2 (&Ain)[CSA], double2 (&B)[CSB], PhaseSt &st,
+                                        int *ipos, double2 *u1, int tid, int team) {
+  using Sh = Shape<S, CS, NW>;
+  constexpr int TS = Sh::TS, RC = Sh::RC;
+  constexpr int NB = S * CSB;
+  const int rr = tid / S, par = tid % S;
+  const uint64_t live = st.live;
+  team_sync<NW, TEAMS>(team);  // the last column's shared-memory reads are done
+  double2 *row = u1 + (size_t)rr * NB;
+#pragma unroll
+  for (int s = 0; s < CSB; ++s) row[S * s + par] = c0();
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < CSA; ++s) {
+    const int i = ipos[S * s + par];
+    if (i >= 0 && ((live >> i) & 1ull)) row[__popcll(live & ((1ull << i) - 1ull))] = Ain[s];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < CSB; ++s) B[s] = row[S * s + par];
+  team_sync<NW, TEAMS>(team);
+  // new position table, row ownership, and zero pivot-column slots without an owner
+  const int L = __popcll(live);
+  for (int i = tid; i < 64; i += TS) {
+    if ((live >> i) & 1ull) ipos[__popcll(live & ((1ull << i) - 1ull))] = i;
+    if (i >= L) ipos[i] = -1;
+  }
+  st.mypos = (rr < 64 && ((live >> rr) & 1ull)) ? __popcll(live & ((1ull << rr) - 1ull)) : -1;
+  st.livec = live;
+  double2 *kbuf = u1 + 2 * NW * Sh::CC;
+  for (int q = L + tid; q < RC; q += TS) {
+    kbuf[q] = c0();
+    kbuf[RC + q] = c0();
+  }
+  team_sync<NW, TEAMS>(team);
+}
+
+template <int S, int CS, int NW, int TEAMS>
+__device__ __forceinline__ void reduce_phased(double2 (&A)[CS], int &label, double2 &colv, int E,
+                                              int NTL, double2 *hb, double2 *u1, int *ipos, int tid,
+                                              int team) {
+  using Sh = Shape<S, CS, NW>;
+  constexpr int TS = Sh::TS;
+  constexpr int CS2 = (3 * CS + 3) / 4, CS3 = (CS + 1) / 2, CS4 = (CS + 3) / 4;
+  const int lane = tid & 31, rr = tid / S, par = tid % S;
+  PhaseSt st;
+  st.label = label;
+  st.colv = colv;
+  st.buf = 0;
+  st.mypos = rr;
+  st.live = (E >= 64 ? ~0ull : ((1ull << E) - 1ull)) & ~1ull;
+  st.livec = (E >= 64 ? ~0ull : ((1ull << E) - 1ull));
+  for (int q = tid; q < 64; q += TS) ipos[q] = (q < E) ? q : -1;
+  team_sync<NW, TEAMS>(team);
+  const int kend = E >= 2 ? E - 2 : 0;
+  const int k2 = min(kend, max(0, E - 1 - S * CS2));
+  const int k3 = max(k2, min(kend, max(0, E - 1 - S * CS3)));
+  const int k4 = max(k3, min(kend, max(0, E - 1 - S * CS4)));
+  phase_steps<S, CS, CS, NW, TEAMS>(A, st, 0, k2, E, NTL, hb, u1, tid, team);
+  double2 A2[CS2];
+  compact<S, CS, CS, CS2, NW, TEAMS>(A, A2, st, ipos, u1, tid, team);
+  phase_steps<S, CS, CS2, NW, TEAMS>(A2, st, k2, k3, E, NTL, hb, u1, tid, team);
+  double2 A3[CS3];
+  compact<S, CS, CS2, CS3, NW, TEAMS>(A2, A3, st, ipos, u1, tid, team);
+  phase_steps<S, CS, CS3, NW, TEAMS>(A3, st, k3, k4, E, NTL, hb, u1, tid, team);
+  double2 A4[CS4];
+  compact<S, CS, CS3, CS4, NW, TEAMS>(A3, A4, st, ipos, u1, tid, team);
+  phase_steps<S, CS, CS4, NW, TEAMS>(A4, st, k4, kend, E, NTL, hb, u1, tid, team);
+  // the last two columns: the carried one (label kend) and the last live one
+  const int lb = st.label;
+  if (E >= 1) {
+    if (par == 0 && lb < E && kend + 1 - lb < NTL) hb[lb * NTL + kend + 1 - lb] = st.colv;
+    if (E >= 2) {
+      const int pl = __ffsll((long long)st.live) - 1;  // label E-1
+      const int pos = __popcll(st.livec & ((1ull << pl) - 1ull));
+      const double2 cl = read_col<S, CS4>(A4, pos, lane);
+      if (par == 0 && lb < E && E - lb < NTL) hb[lb * NTL + E - lb] = cl;
+    }
+  }
+  label = st.label;
+  colv = st.colv;
+}
+
 // ================================================================ one term, one team
 // g(t) of one term (valid in warp 0 of the team); sign and weight from the decode (warp 0).
 // CMP: keep the live columns contiguous (compaction) and skip finished slot groups.
@@ -426,110 +607,7 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
   int buf = 0;
   const int kend = E >= 2 ? E - 2 : 0;
   if constexpr (CMP) {
-    // live column positions are [lo, E); the lowest live column moves into the position the
-    // pivot column frees; slot groups of 4 below lo are skipped with a uniform branch
-    constexpr int NG = (CS + 3) / 4;
-    int lo = 1;
-    int mypos = rr;  // position of this index's column while it is live, else -1
-    for (int k = 0; k < kend; ++k) {
-      double2 *cb = cand + buf * NW * CC;
-      double2 *kb = kbuf + buf * RC;
-      unsigned *yk = keys + buf * NW * 4;
-      double2 *yv = reinterpret_cast<double2 *>(keys + 2 * NW * 4) + buf * NW;
-      buf ^= 1;
-      const int glo = lo / (4 * S);
-      const bool candr = label > k && label < E;
-      unsigned key = 0u;
-      if (candr) {
-        const unsigned fbits = __float_as_uint((float)(fabs(colv.x) + fabs(colv.y)));
-        key = (((fbits >> 6) + 1u) << 6) | (unsigned)(63 - label);
-      }
-      const unsigned wkey = __reduce_max_sync(LHAF_FULL, key);
-      if (par == 0 && mypos >= 0) kb[mypos] = candr ? colv : c0();
-      if (tid < lo - 4 * S * glo) kb[4 * S * glo + tid] = c0();  // dead head of the first group
-      if (candr && key == wkey) {
-        double2 *dst = cb + warp * CC + par;
-#pragma unroll
-        for (int g = 0; g < NG; ++g)
-          if (g >= glo) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (4 * g + i < CS) dst[S * (4 * g + i)] = A[4 * g + i];
-          }
-        if (par == 0) {
-          yv[warp] = colv;
-          yk[4 * warp + 1] = (unsigned)rr;
-          yk[4 * warp + 2] = (unsigned)mypos;
-        }
-      }
-      if (lane == 0) yk[4 * warp] = wkey;
-      team_sync<NW, TEAMS>(team);
-
-      unsigned bkey = 0u;
-      int wb = 0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const unsigned kw = yk[4 * w];
-        if (kw > bkey) { bkey = kw; wb = w; }
-      }
-      const int plabel = 63 - (int)(bkey & 63u);
-      const int p = (int)yk[4 * wb + 1];
-      const int qp = (int)yk[4 * wb + 2];  // column position of the pivot index
-      const int newlabel = (rr == p) ? k + 1 : (label == k + 1 ? plabel : label);
-      if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL) hb[newlabel * NTL + k + 1 - newlabel] = colv;
-      if ((bkey >> 6) > 1u) {
-        const double2 piv = yv[wb];
-        const double2 ip = crecip(piv);
-        const double2 m = (candr && rr != p) ? cmul(colv, ip) : c0();
-        const double2 *rp = cb + wb * CC + par;
-        const double2 *kq = kb + par;
-        double xr0 = 0, xi0 = 0, yr0 = 0, yi0 = 0, xr1 = 0, xi1 = 0, yr1 = 0, yi1 = 0;
-#pragma unroll
-        for (int g = 0; g < NG; ++g)
-          if (g >= glo) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int s = 4 * g + i;
-              if (s < CS) {
-                const double2 r = rp[S * s];
-                const double2 q = kq[S * s];
-                double2 a = cfms(m, r, A[s]);
-                A[s] = a;
-                if (s & 1) {
-                  xr1 = fma(a.x, q.x, xr1); xi1 = fma(a.y, q.y, xi1);
-                  yr1 = fma(a.x, q.y, yr1); yi1 = fma(a.y, q.x, yi1);
-                } else {
-                  xr0 = fma(a.x, q.x, xr0); xi0 = fma(a.y, q.y, xi0);
-                  yr0 = fma(a.x, q.y, yr0); yi0 = fma(a.y, q.x, yi0);
-                }
-              }
-            }
-          }
-        double2 sum = make_double2((xr0 + xr1) - (xi0 + xi1), (yr0 + yr1) + (yi0 + yi1));
-#pragma unroll
-        for (int x = 1; x < S; x <<= 1) sum = cadd(sum, shfl2_xor(sum, x));
-        colv = cmul(sum, ip);
-      } else {
-        colv = read_pos<S, CS>(A, qp, lane);  // nothing to eliminate: column p as it stands
-      }
-      // compaction: the column at position lo moves into the pivot column's position
-      if (qp != lo) {
-        const double2 x = read_pos<S, CS>(A, lo, lane);
-        if (par == qp % S) wr_sw<CS>(A, qp / S, x);
-        if (mypos == lo) mypos = qp;
-      }
-      if (rr == p) mypos = -1;
-      lo += 1;
-      label = newlabel;
-    }
-    // the last two columns: the carried one (label kend) and the last live one (position lo)
-    if (E >= 1) {
-      if (par == 0 && label < E && kend + 1 - label < NTL) hb[label * NTL + kend + 1 - label] = colv;
-      if (E >= 2) {
-        const double2 cl = read_pos<S, CS>(A, lo, lane);
-        if (par == 0 && label < E && E - label < NTL) hb[label * NTL + E - label] = cl;
-      }
-    }
+    reduce_phased<S, CS, NW, TEAMS>(A, label, colv, E, NTL, hb, T.u1, T.wv, tid, team);
   } else {
   uint64_t live = (E >= 64 ? ~0ull : ((1ull << E) - 1ull)) & ~1ull;  // indices with label > k
   for (int k = 0; k < kend; ++k) {
@@ -782,20 +860,22 @@ struct Inst {
 // warp of R registers allows floor(512 / R) warps per sub-partition.
 using I9 = Inst<1, 9, 1, 4, 128>;
 using I17 = Inst<1, 17, 1, 4, 128>;
-using I25 = Inst<1, 25, 1, 4, 168>;
-using I32 = Inst<1, 32, 1, 4, 168>;
-using I48 = Inst<2, 24, 3, 1, 168>;
-using D48 = Inst<2, 24, 3, 1, 255>;  // (LHAF_V3_ALT=4)
-using I62 = Inst<2, 31, 4, 1, 255>;  // 2 CTAs / SM (2 warps per 16K-register sub-partition)
-using I64 = Inst<2, 32, 4, 1, 168>;
+using I25 = Inst<1, 25, 1, 4, 168, true>;
+using I32 = Inst<1, 32, 1, 4, 168, true>;
+using I48 = Inst<2, 24, 3, 1, 168, true>;
+using I62 = Inst<2, 31, 4, 1, 232, true>;  // 2 CTAs / SM (2 warps per 16K-register sub-partition)
+using I64 = Inst<2, 32, 4, 1, 168, true>;
 // alternatives (LHAF_V3_ALT=1): more lanes per row, fewer registers, more warps per SM
 using A26 = Inst<2, 13, 2, 2, 104>;   // E <= 26: 4 warps / CTA
 using A48 = Inst<4, 12, 6, 1, 104>;   // E <= 48: 6 warps / CTA
 using A64 = Inst<4, 16, 8, 1, 128>;   // E <= 64: 8 warps / CTA
-using B62 = Inst<2, 31, 4, 1, 232>;   // (LHAF_V3_ALT=2) E <= 62, 232 registers
-using C25 = Inst<1, 25, 1, 4, 168, true>;  // (LHAF_V3_ALT=3) compaction variants
-using C48 = Inst<2, 24, 3, 1, 168, true>;
-using C62 = Inst<2, 31, 4, 1, 232, true>;
+// (LHAF_V3_ALT=3) single-phase reduction (no compaction)
+using P25 = Inst<1, 25, 1, 4, 168>;
+using P48 = Inst<2, 24, 3, 1, 168>;
+using P62 = Inst<2, 31, 4, 1, 255>;
+// (LHAF_V3_ALT=5) phased reduction at 255 registers
+using R48 = Inst<2, 24, 3, 1, 255, true>;
+using R62 = Inst<2, 31, 4, 1, 255, true>;
 static int alt_mode() {
   static const int m = [] { const char *e = getenv("LHAF_V3_ALT"); return e ? atoi(e) : 0; }();
   return m;
@@ -825,12 +905,14 @@ extern "C" int lhaf_debug_phase_cycles(unsigned long long *out8) {
 #endif
 
 #define LHAF_V3_DISPATCH(CALL)                  \
-  if (v3::alt_mode() == 2 && E > 48 && E <= v3::B62::EMAX) return v3::B62::CALL; \
-  if (v3::alt_mode() == 4 && E > 32 && E <= v3::D48::EMAX) return v3::D48::CALL; \
   if (v3::alt_mode() == 3) {                    \
-    if (E > 17 && E <= v3::C25::EMAX) return v3::C25::CALL; \
-    if (E > 32 && E <= v3::C48::EMAX) return v3::C48::CALL; \
-    if (E > 48 && E <= v3::C62::EMAX) return v3::C62::CALL; \
+    if (E > 17 && E <= v3::P25::EMAX) return v3::P25::CALL; \
+    if (E > 32 && E <= v3::P48::EMAX) return v3::P48::CALL; \
+    if (E > 48 && E <= v3::P62::EMAX) return v3::P62::CALL; \
+  }                                             \
+  if (v3::alt_mode() == 5) {                    \
+    if (E > 32 && E <= v3::R48::EMAX) return v3::R48::CALL; \
+    if (E > 48 && E <= v3::R62::EMAX) return v3::R62::CALL; \
   }                                             \
   if (v3::alt_mode() == 1) {                    \
     if (E <= v3::A26::EMAX && E > 17) return v3::A26::CALL; \
