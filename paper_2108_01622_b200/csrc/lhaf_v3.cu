@@ -199,25 +199,23 @@ __device__ __forceinline__ void labudde(const double2 *hb, double2 *Q, int E, in
   }
   __syncwarp();
   for (int j = E - 1; j >= 0; --j) {
-    // S_{j-1}[t] from rows j+1 .. E (final)
+    // S_{j-1}[t] from rows j+1 .. E (final); groups of 4 terms under a warp-uniform bound
     double2 Sn[NRT];
 #pragma unroll
     for (int r = 0; r < NRT; ++r) {
       const int t = lane + 32 * r;
       double2 a0 = c0(), a1 = c0(), a2 = c0(), a3 = c0();
-      if (j >= 1 && t < NTL && t <= E - j + 1) {
+      const int mm = (j >= 1 && t < NTL && t <= E - j + 1) ? min(t - 1, E - j) : 0;
+      const int mw = min(min(NTL, 32 * (r + 1)) - 2, E - j);  // max of mm over the warp
+      if (j >= 1) {
         const double2 *F = hb + (j - 1) * NTL + 1;  // F_{j-1}[m] = F[m]
-        const int mm = min(t - 1, E - j);
         const double2 *qd = Q + (j + 1) * NTL + t - 2;  // q_{j+m}[t-m-1] at m = 1
-        int m = 1;
-        for (; m + 3 <= mm; m += 4) {
-          a0 = cfma(F[m], qd[0], a0);
-          a1 = cfma(F[m + 1], qd[NTL - 1], a1);
-          a2 = cfma(F[m + 2], qd[2 * (NTL - 1)], a2);
-          a3 = cfma(F[m + 3], qd[3 * (NTL - 1)], a3);
-          qd += 4 * (NTL - 1);
+        for (int m = 1; m <= mw; m += 4, qd += 4 * (NTL - 1)) {
+          if (m <= mm) a0 = cfma(F[m], qd[0], a0);
+          if (m + 1 <= mm) a1 = cfma(F[m + 1], qd[NTL - 1], a1);
+          if (m + 2 <= mm) a2 = cfma(F[m + 2], qd[2 * (NTL - 1)], a2);
+          if (m + 3 <= mm) a3 = cfma(F[m + 3], qd[3 * (NTL - 1)], a3);
         }
-        for (; m <= mm; ++m, qd += NTL - 1) a0 = cfma(F[m], qd[0], a0);
       }
       Sn[r] = make_double2(-((a0.x + a1.x) + (a2.x + a3.x)), -((a0.y + a1.y) + (a2.y + a3.y)));
     }
@@ -265,19 +263,22 @@ __device__ __forceinline__ void labudde_team(const double2 *hb, double2 *Q, doub
 #pragma unroll
     for (int r = 0; r < NRT; ++r) {
       const int t = lane + 32 * r;
-      double2 a0 = c0(), a1 = c0();
-      if (j >= 1 && t < NTL && t <= E - j + 1) {
+      double2 a0 = c0(), a1 = c0(), a2 = c0(), a3 = c0();
+      const int mm = (j >= 1 && t < NTL && t <= E - j + 1) ? min(t - 1, E - j) : 0;
+      const int mw = min(min(NTL, 32 * (r + 1)) - 2, E - j);  // max of mm over the warp
+      if (j >= 1) {
         const double2 *F = hb + (j - 1) * NTL + 1;  // F_{j-1}[m] = F[m]
-        const int mm = min(t - 1, E - j);
         int m = 1 + warp;
         const double2 *qd = Q + (j + m) * NTL + t - m - 1;  // q_{j+m}[t-m-1]
-        for (; m + NW <= mm; m += 2 * NW) {
-          a0 = cfma(F[m], qd[0], a0);
-          a1 = cfma(F[m + NW], qd[NW * (NTL - 1)], a1);
-          qd += 2 * NW * (NTL - 1);
+        for (; m <= mw; m += 4 * NW, qd += 4 * NW * (NTL - 1)) {  // warp-uniform bound
+          if (m <= mm) a0 = cfma(F[m], qd[0], a0);
+          if (m + NW <= mm) a1 = cfma(F[m + NW], qd[NW * (NTL - 1)], a1);
+          if (m + 2 * NW <= mm) a2 = cfma(F[m + 2 * NW], qd[2 * NW * (NTL - 1)], a2);
+          if (m + 3 * NW <= mm) a3 = cfma(F[m + 3 * NW], qd[3 * NW * (NTL - 1)], a3);
         }
-        if (m <= mm) a0 = cfma(F[m], qd[0], a0);
       }
+      a0 = cadd(a0, a2);
+      a1 = cadd(a1, a3);
       if (t < NTL) pw[t] = cadd(a0, a1);
     }
     if (warp == 0) {
