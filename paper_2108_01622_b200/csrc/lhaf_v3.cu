@@ -1,32 +1,30 @@
 // lhaf_v3.cu -- variant 3 of the sieve kernel (the default): register-resident rows,
-// Gauss-transform Hessenberg reduction of the bordered matrix with a branch-free per-column
-// body, a team-parallel trailing La Budde on the band of H, and the power series of each term
-// pipelined into the next term's reduction.  DESIGN.md "Kernel v3"; SURVEY 8(a) rows a4-a11.
+// Gauss-transform Hessenberg reduction of the bordered matrix in four register phases of
+// shrinking width, a team-parallel trailing La Budde on the band of H, and the power series.
+// DESIGN.md "Kernel v3"; SURVEY 8(a) rows a4-a11.
 //
 // One "team" of 32*NW threads evaluates one sieve term at a time; a CTA holds TEAMS teams.
 //   a4  decode t -> w_h = eta_h - 2 k_h, sign (-1)^{sum k}, weight prod C(eta_h, k_h)
 //   a5  B = [[0, z^T], [y, M]] with M = C X_w, y = v, z^T = v X_w (loops present), else B = M.
 //       Row r of B lives in the registers of S threads; slot s of thread (r, par) holds column
-//       S*s + par.
+//       position S*s + par.
 //   a6  Hessenberg reduction of B by Gauss transforms with partial pivoting, index 0 fixed
 //       (so the first step maps y -> beta e1 and carries z^T -> z^T L^{-1}: the "bordered"
 //       loop trick).  Rows and columns never move: index i gets its final Hessenberg position
 //       as a label.  Per column k one team barrier:
 //         pivot = warp REDUX-max of a packed (|B[r][k]|_1, label) key, then across warps;
 //         each warp's best row is published to smem; every row then does, in ONE fused pass
-//         over all its slots,
+//         over its live slots,
 //             left   A[r][c] -= m_r A[p][c]          (m_r = B[r][k] / piv, 0 if r is done)
 //             right  acc     += A[r][c] B[c][k]      (B[c][k] = 0 unless c is remaining)
-//         and the new pivot column p = acc / piv is carried in registers (never stored).
-//       Columns of finished indices are left as garbage (they are multiplied by zero).
-//       Finished columns go to the band hb (H[j][j-1 .. j+NTL-2]).
-//   a7  F_j[m] = H[j][j+m] prod_{i=1..m} H[j+i][j+i-1]; trailing La Budde on the top
-//       NTL = n+2 coefficients of q_j(x) = det(x I - H[j:, j:]) (c_B = q_0, c_M = q_1), the
-//       m-sums split across the team's warps (one barrier per j).
+//         and the new pivot column p = acc (scaled by piv: unit subdiagonal) is carried in
+//         registers.  At 3/4, 1/2 and 1/4 of the live columns the rows are compacted into
+//         narrower register arrays (reduce_phased).  Finished columns go to the band hb.
+//   a7  trailing La Budde on the top NTL = n+2 coefficients of q_j(x) = det(x I - H[j:, j:])
+//       (c_B = q_0, c_M = q_1), the m-sums split across the team's warps (one barrier per j).
 //   a8  loop terms: lam S(lam) = 1 - c_B / c_M, S = sum_j s_j lam^j, s_j = z^T M^{j-1} y.
 //   a9  g = [lam^n] c_M^{-1/2} exp(S/2)   (the paper's f with X -> X_w, reading C4):
-//       a column-sweep series program of ~2n steps, run by the team's last warp one or two
-//       steps per column of the NEXT term's reduction (drained at the end of a work unit).
+//       column-sweep series recursions in warp 0.
 //   a10 term = (-1)^{sum k} prod C(eta_h, k_h) g, double-double accumulation per work unit.
 #include <cuda_runtime.h>
 #include <algorithm>
@@ -127,7 +125,7 @@ __device__ __forceinline__ void team_sync(int team) {
 }
 
 // Shared memory of one team (double2 words), for a pattern with (E, NTL, n):
-//   hb   [E][NTL]       band of H: [j][0] = H[j][j-1], [j][1] = H[j][j], [j][1+m] = H[j][j+m]
+//   hb   [E][NTL]       band of H (unit subdiagonal): [j][1] = H[j][j], [j][1+m] = H[j][j+m]
 //   u1   union { cand [2][NW][CC] | kb [2][RC] | keys [2][NW] | piv [2][NW] } (reduction)
 //        union { Q [E+1][NTL] | Qs, Rs, Es [n+2] | part [2][NW][NTL] }         (La Budde, series)
 //   w    64 ints, then 64 doubles of column weights
@@ -385,7 +383,8 @@ __device__ __forceinline__ double2 series(const double2 *cM, const double2 *cB, 
 // positions 0..L-1 (ascending index order), so later phases sweep CS2 = 3CS/4, CS3 = CS/2,
 // CS4 = CS/4 slots instead of CS.  kb and the published pivot rows are indexed by position.
 struct PhaseSt {
-  int label, buf, mypos;
+  int label, buf, mypos, zl;  // zl: 1 + the label after the latest zero subdiagonal (0: none)
+  double2 rs;                 // row scale (see team_term)
   uint64_t live, livec;  // indices with label > k; the live set at the last compaction
   double2 colv;
 };
@@ -438,7 +437,8 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
     const int p = (int)yk[4 * wb + 1];   // pivot: physical index
     const int qp = (int)yk[4 * wb + 2];  // and its column position
     const int newlabel = (rr == p) ? k + 1 : (st.label == k + 1 ? plabel : st.label);
-    if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL) hb[newlabel * NTL + k + 1 - newlabel] = st.colv;
+    if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL)
+      hb[newlabel * NTL + k + 1 - newlabel] = (newlabel < st.zl) ? c0() : cmul(st.rs, st.colv);
     st.live &= ~(1ull << p);
     if ((bkey >> 6) > 1u) {
       const double2 ip = (NW > 1) ? yv[2 * wb + 1] : crecip(yv[2 * wb]);
@@ -463,40 +463,44 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
       double2 sum = make_double2((xr0 + xr1) - (xi0 + xi1), (yr0 + yr1) + (yi0 + yi1));
 #pragma unroll
       for (int x = 1; x < S; x <<= 1) sum = cadd(sum, shfl2_xor(sum, x));
-      st.colv = cmul(sum, ip);
+      st.colv = sum;  // column p scaled by the pivot: unit subdiagonal
+      if (rr == p) st.rs = ip;
     } else {
       st.colv = read_col<S, CSP>(A, qp, lane);  // nothing to eliminate: column p as it stands
+      st.zl = k + 1;                            // H[k+1][k] = 0
     }
     st.label = newlabel;
   }
 }
 
 // Compaction of every row's live columns from CSA to CSB slots (see above).  ipos[q] = index
-// of the column at position q (-1: none).
+// of the column at position q (-1: none); npos = the new position of each old one.
 template <int S, int CS, int CSA, int CSB, int NW, int TEAMS>
 __device__ __forceinline__ void compact(const double2 (&Ain)[CSA], double2 (&B)[CSB], PhaseSt &st,
-                                        int *ipos, double2 *u1, int tid, int team) {
+                                        int *ipos, int *npos, double2 *u1, int tid, int team) {
   using Sh = Shape<S, CS, NW>;
   constexpr int TS = Sh::TS, RC = Sh::RC;
   constexpr int NB = S * CSB;
   const int rr = tid / S, par = tid % S;
   const uint64_t live = st.live;
-  team_sync<NW, TEAMS>(team);  // the last column's shared-memory reads are done
+  const int L = __popcll(live);
+  for (int q = tid; q < 64; q += TS) {
+    const int i = ipos[q];
+    npos[q] = (i >= 0 && ((live >> i) & 1ull)) ? __popcll(live & ((1ull << i) - 1ull)) : -1;
+  }
+  team_sync<NW, TEAMS>(team);  // npos visible; the last column's shared-memory reads are done
   double2 *row = u1 + (size_t)rr * NB;
 #pragma unroll
-  for (int s = 0; s < CSB; ++s) row[S * s + par] = c0();
-  __syncwarp();
-#pragma unroll
   for (int s = 0; s < CSA; ++s) {
-    const int i = ipos[S * s + par];
-    if (i >= 0 && ((live >> i) & 1ull)) row[__popcll(live & ((1ull << i) - 1ull))] = Ain[s];
+    const int np = npos[S * s + par];
+    if (np >= 0) row[np] = Ain[s];
   }
   __syncwarp();
 #pragma unroll
-  for (int s = 0; s < CSB; ++s) B[s] = row[S * s + par];
+  for (int s = 0; s < CSB; ++s) B[s] = (S * s + par < L) ? row[S * s + par] : c0();
   team_sync<NW, TEAMS>(team);
-  // new position table, row ownership, and zero pivot-column slots without an owner
-  const int L = __popcll(live);
+  // new position table, row ownership, and zero pivot-column slots without an owner (the next
+  // column's barrier orders these writes before their readers)
   for (int i = tid; i < 64; i += TS) {
     if ((live >> i) & 1ull) ipos[__popcll(live & ((1ull << i) - 1ull))] = i;
     if (i >= L) ipos[i] = -1;
@@ -508,13 +512,12 @@ __device__ __forceinline__ void compact(const double2 (&Ain)[CSA], double2 (&B)[
     kbuf[q] = c0();
     kbuf[RC + q] = c0();
   }
-  team_sync<NW, TEAMS>(team);
 }
 
 template <int S, int CS, int NW, int TEAMS>
 __device__ __forceinline__ void reduce_phased(double2 (&A)[CS], int &label, double2 &colv, int E,
-                                              int NTL, double2 *hb, double2 *u1, int *ipos, int tid,
-                                              int team) {
+                                              int NTL, double2 *hb, double2 *u1, int *ipos,
+                                              int *npos, double2 *betap, int tid, int team) {
   using Sh = Shape<S, CS, NW>;
   constexpr int TS = Sh::TS;
   constexpr int CS2 = (3 * CS + 3) / 4, CS3 = (CS + 1) / 2, CS4 = (CS + 3) / 4;
@@ -524,6 +527,8 @@ __device__ __forceinline__ void reduce_phased(double2 (&A)[CS], int &label, doub
   st.colv = colv;
   st.buf = 0;
   st.mypos = rr;
+  st.zl = 0;
+  st.rs = c1();
   st.live = (E >= 64 ? ~0ull : ((1ull << E) - 1ull)) & ~1ull;
   st.livec = (E >= 64 ? ~0ull : ((1ull << E) - 1ull));
   for (int q = tid; q < 64; q += TS) ipos[q] = (q < E) ? q : -1;
@@ -534,23 +539,25 @@ __device__ __forceinline__ void reduce_phased(double2 (&A)[CS], int &label, doub
   const int k4 = max(k3, min(kend, max(0, E - 1 - S * CS4)));
   phase_steps<S, CS, CS, NW, TEAMS>(A, st, 0, k2, E, NTL, hb, u1, tid, team);
   double2 A2[CS2];
-  compact<S, CS, CS, CS2, NW, TEAMS>(A, A2, st, ipos, u1, tid, team);
+  compact<S, CS, CS, CS2, NW, TEAMS>(A, A2, st, ipos, npos, u1, tid, team);
   phase_steps<S, CS, CS2, NW, TEAMS>(A2, st, k2, k3, E, NTL, hb, u1, tid, team);
   double2 A3[CS3];
-  compact<S, CS, CS2, CS3, NW, TEAMS>(A2, A3, st, ipos, u1, tid, team);
+  compact<S, CS, CS2, CS3, NW, TEAMS>(A2, A3, st, ipos, npos, u1, tid, team);
   phase_steps<S, CS, CS3, NW, TEAMS>(A3, st, k3, k4, E, NTL, hb, u1, tid, team);
   double2 A4[CS4];
-  compact<S, CS, CS3, CS4, NW, TEAMS>(A3, A4, st, ipos, u1, tid, team);
+  compact<S, CS, CS3, CS4, NW, TEAMS>(A3, A4, st, ipos, npos, u1, tid, team);
   phase_steps<S, CS, CS4, NW, TEAMS>(A4, st, k4, kend, E, NTL, hb, u1, tid, team);
   // the last two columns: the carried one (label kend) and the last live one
   const int lb = st.label;
   if (E >= 1) {
-    if (par == 0 && lb < E && kend + 1 - lb < NTL) hb[lb * NTL + kend + 1 - lb] = st.colv;
+    if (par == 0 && lb < E && kend + 1 - lb < NTL)
+      hb[lb * NTL + kend + 1 - lb] = (lb < st.zl) ? c0() : cmul(st.rs, st.colv);
     if (E >= 2) {
       const int pl = __ffsll((long long)st.live) - 1;  // label E-1
+      if (rr == pl && par == 0) *betap = st.colv;     // H[E-1][E-2], not yet scaled to 1
       const int pos = __popcll(st.livec & ((1ull << pl) - 1ull));
       const double2 cl = read_col<S, CS4>(A4, pos, lane);
-      if (par == 0 && lb < E && E - lb < NTL) hb[lb * NTL + E - lb] = cl;
+      if (par == 0 && lb < E && E - lb < NTL) hb[lb * NTL + E - lb] = (lb < st.zl) ? c0() : cmul(st.rs, cl);
     }
   }
   label = st.label;
@@ -599,7 +606,12 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
   }
   LHAF_PHASE(0)
 
-  // ---- a6: Gauss-transform Hessenberg reduction, one barrier per column
+  // ---- a6: Gauss-transform Hessenberg reduction, one barrier per column.  Each step is
+  // followed by the diagonal similarity that scales the new pivot column by the pivot and the
+  // pivot row by its inverse, so H has a unit subdiagonal (0 after a zero pivot) and La Budde
+  // needs no subdiagonal products.  The row scaling is not applied to the registers: a pivot
+  // row keeps rs = 1/pivot and multiplies its band entries by it; after a zero pivot at step
+  // k, band entries of rows above k+1 in later columns are 0 (zl).
   double2 *cand = T.u1;                                       // [2][NW][CC]
   double2 *kbuf = cand + 2 * NW * CC;                         // [2][RC]
   unsigned *keys = reinterpret_cast<unsigned *>(kbuf + 2 * RC);  // [2][NW][4] (key, phys)
@@ -607,10 +619,14 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
   double2 colv = (S == 1) ? A[0] : shfl2(A[0], lane & ~(S - 1));    // this row's B[.][k]
   int buf = 0;
   const int kend = E >= 2 ? E - 2 : 0;
+  double2 *betap = reinterpret_cast<double2 *>(T.ww) + 31;  // (past npos: 64 ints)
   if constexpr (CMP) {
-    reduce_phased<S, CS, NW, TEAMS>(A, label, colv, E, NTL, hb, T.u1, T.wv, tid, team);
+    reduce_phased<S, CS, NW, TEAMS>(A, label, colv, E, NTL, hb, T.u1, T.wv,
+                                    reinterpret_cast<int *>(T.ww), betap, tid, team);
   } else {
   uint64_t live = (E >= 64 ? ~0ull : ((1ull << E) - 1ull)) & ~1ull;  // indices with label > k
+  int zl = 0;
+  double2 rs = c1();
   for (int k = 0; k < kend; ++k) {
     double2 *cb = cand + buf * NW * CC;
     double2 *kb = kbuf + buf * RC;
@@ -653,7 +669,8 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
     const int p = (int)yk[4 * wb + 1];  // pivot: physical index
     const int newlabel = (rr == p) ? k + 1 : (label == k + 1 ? plabel : label);
     // finished column k: H[label][k] for rows with label <= k + 1
-    if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL) hb[newlabel * NTL + k + 1 - newlabel] = colv;
+    if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL)
+      hb[newlabel * NTL + k + 1 - newlabel] = (newlabel < zl) ? c0() : cmul(rs, colv);
     live &= ~(1ull << p);
     if ((bkey >> 6) > 1u) {  // nonzero pivot
       const double2 ip = (NW > 1) ? yv[2 * wb + 1] : crecip(yv[2 * wb]);
@@ -679,37 +696,34 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
       double2 sum = make_double2((xr0 + xr1) - (xi0 + xi1), (yr0 + yr1) + (yi0 + yi1));
 #pragma unroll
       for (int x = 1; x < S; x <<= 1) sum = cadd(sum, shfl2_xor(sum, x));
-      colv = cmul(sum, ip);
+      colv = sum;  // column p scaled by the pivot: unit subdiagonal
+      if (rr == p) rs = ip;
     } else {
       colv = read_col<S, CS>(A, p, lane);  // nothing to eliminate: column p as it stands
+      zl = k + 1;                          // H[k+1][k] = 0
     }
     label = newlabel;
     LHAF_PHASE(1)
   }
   // the last two columns: the carried one (label kend) and the remaining live index
   if (E >= 1) {
-    if (par == 0 && label < E && kend + 1 - label < NTL) hb[label * NTL + kend + 1 - label] = colv;
+    if (par == 0 && label < E && kend + 1 - label < NTL)
+      hb[label * NTL + kend + 1 - label] = (label < zl) ? c0() : cmul(rs, colv);
     if (E >= 2) {
       const int pl = __ffsll((long long)live) - 1;  // label E-1
+      if (rr == pl && par == 0) *betap = colv;        // H[E-1][E-2], not yet scaled to 1
       const double2 cl = read_col<S, CS>(A, pl, lane);
-      if (par == 0 && label < E && E - label < NTL) hb[label * NTL + E - label] = cl;
+      if (par == 0 && label < E && E - label < NTL) hb[label * NTL + E - label] = (label < zl) ? c0() : cmul(rs, cl);
     }
   }
   }
   team_sync<NW, TEAMS>(team);
+  // the last subdiagonal: scale column E-1 by it (rows above E-1; La Budde's first barrier
+  // orders these writes before its reads)
+  if (E >= 2 && par == 0 && label < E - 1 && E - label < NTL)
+    hb[label * NTL + E - label] = cmul(hb[label * NTL + E - label], *betap);
   LHAF_PHASE(1)
 
-  // ---- a7: F_j[m] = H[j][j+m] prod_{i=1..m} H[j+i][j+i-1] in place
-  if (par == 0 && label < E) {
-    double2 pi = c1();
-    const int mmax = min(NTL - 2, E - 1 - label);
-    for (int m = 1; m <= mmax; ++m) {
-      pi = cmul(pi, hb[(label + m) * NTL]);
-      hb[label * NTL + 1 + m] = cmul(hb[label * NTL + 1 + m], pi);
-    }
-  }
-  team_sync<NW, TEAMS>(team);
-  LHAF_PHASE(2)
   double2 g = c0();
   double2 *Q = T.u1;  // [E+1][NTL]: Q[j][t] = coefficient of x^{deg q_j - t}
   {

@@ -1,5 +1,5 @@
 """Phase breakdown of the v3 kernel (diagnostic build with -DLHAF_PHASE_TIMING): cycles of
-thread 0 of each team in decode/build, reduction, band->F, La Budde, series, end barrier.
+thread 0 of each team in decode/build, reduction, (unused), La Budde, series, end barrier.
     python tools/phase_timing.py build        (here: compiles tools/_diag/liblhaf_timing.so)
     python tools/phase_timing.py run [cfg]    (GPU box)"""
 import ctypes, os, sys
@@ -26,7 +26,7 @@ for c in [int(x) for x in sys.argv[2:]] or [2, 4, 5]:
     job.reset(); job.run(0, U); torch.cuda.synchronize()
     lib.lhaf_debug_phase_cycles(buf)
     terms = job.terms * U / job.units
-    names = ["decode+build", "column: update+carry", "band->F", "La Budde", "series", "end barrier",
+    names = ["decode+build", "column: update+carry", "(unused)", "La Budde", "series", "end barrier",
              "column: pivot+publish", "column: barrier wait"]
     tot = sum(buf[i] for i in range(8))
     print(f"cfg{c}: terms={terms:.0f} cycles/term (thread 0 of each team): " +
