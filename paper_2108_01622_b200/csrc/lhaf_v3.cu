@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include "lhaf_device.cuh"
 
 namespace lhaf {
@@ -127,7 +128,7 @@ __device__ __forceinline__ void team_sync(int team) {
 // Shared memory of one team (double2 words), for a pattern with (E, NTL, n):
 //   hb   [E][NTL]       band of H (unit subdiagonal): [j][1] = H[j][j], [j][1+m] = H[j][j+m]
 //   u1   union { cand [2][NW][CC] | kb [2][RC] | keys [2][NW] | piv [2][NW] } (reduction)
-//        union { Q [E+1][NTL] | Qs, Rs, Es [n+2] | part [2][NW][NTL] }         (La Budde, series)
+//        union { Q [E+1][NTL] | Qs, Rs, Es [n+2] | part [2][NW][2][NTL] }      (La Budde, series)
 //   w    64 ints, then 64 doubles of column weights
 template <int S, int CS, int NW>
 struct Shape {
@@ -135,7 +136,7 @@ struct Shape {
   static constexpr int EMAX = RC < CC ? RC : CC;
   __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 6 * NW; }
   __host__ __device__ static int u1_words(int E, int NTL, int n) {
-    const int lab = (E + 1) * NTL + 3 * (n + 2) + 2 * NW * NTL;
+    const int lab = (E + 1) * NTL + 3 * (n + 2) + 4 * NW * NTL;
     const int cmp = RC * S * ((3 * CS + 3) / 4);  // phased reduction buffer
     int w = red_words() > lab ? red_words() : lab;
     return w > cmp ? w : cmp;
@@ -302,6 +303,120 @@ __device__ __forceinline__ void labudde_team(const double2 *hb, double2 *Q, doub
         if (t > E - j) q = c0();  // above the degree of q_j
         qn[r] = q;
         if (t < NTL) Q[j * NTL + t] = q;
+      }
+    }
+    team_sync<NW, TEAMS>(team);
+  }
+}
+
+// out[t] = q[t - d] (0 for t < d) over the NRT registers of a warp; d warp-uniform in [1, 31]
+template <int NRT>
+__device__ __forceinline__ void shift_up(const double2 (&q)[NRT], int d, int lane,
+                                         double2 (&out)[NRT]) {
+  double2 sh[NRT];
+#pragma unroll
+  for (int r = 0; r < NRT; ++r) sh[r] = shfl2(q[r], (lane - d) & 31);
+#pragma unroll
+  for (int r = 0; r < NRT; ++r) out[r] = (lane >= d) ? sh[r] : (r == 0 ? c0() : sh[r - 1]);
+}
+
+// Team version, two rows per barrier.  Block b forms rows j = E-1-2b and j-1 in warp 0:
+//   q_j     = q_{j+1} - h_j q_{j+1}[t-1]     - P_j     - F_j[1] q_{j+2}[t-2]
+//   q_{j-1} = q_j     - h_{j-1} q_j[t-1]     - P_{j-1} - F_{j-1}[1] q_{j+1}[t-2]
+//                                                      - F_{j-1}[2] q_{j+2}[t-3]
+// with q_{j+1}, q_{j+2} (the previous block's rows) held in registers, while every warp sums,
+// for the next block's rows r = j-2, j-3, the m-terms on rows >= j+1 (m >= j - r), split
+// m = m0 + w (mod NW): P_r[t] = sum_m F_r[m] q_{r+m+1}[t-m-1] into part[b&1][w][r][t].
+template <int NRT, int NW, int TEAMS>
+__device__ __forceinline__ void labudde_team2(const double2 *hb, double2 *Q, double2 *part, int E,
+                                              int NTL, int warp, int lane, int team) {
+  double2 qa[NRT], qb[NRT];  // q_{j+1}, q_{j+2}
+#pragma unroll
+  for (int r = 0; r < NRT; ++r) {
+    const int t = lane + 32 * r;
+    qa[r] = (t == 0) ? c1() : c0();  // q_E = 1
+    qb[r] = c0();                    // (q_{E+1}: no such row)
+    if (warp == 0 && t < NTL) Q[E * NTL + t] = qa[r];
+    if (t < NTL) {  // the partials of block 0 (none)
+      part[(NW + warp) * 2 * NTL + t] = c0();
+      part[(NW + warp) * 2 * NTL + NTL + t] = c0();
+    }
+  }
+  team_sync<NW, TEAMS>(team);
+  for (int b = 0, j = E - 1; j >= 0; ++b, j -= 2) {
+    // partial m-sums for rows j-2 (slot 0) and j-3 (slot 1) from rows >= j+1 (final)
+    double2 *pw = part + ((b & 1) * NW + warp) * 2 * NTL;
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+      const int rw = j - 2 - sl, m0 = 2 + sl;
+#pragma unroll
+      for (int r = 0; r < NRT; ++r) {
+        const int t = lane + 32 * r;
+        double2 a0 = c0(), a1 = c0(), a2 = c0(), a3 = c0();
+        if (rw >= 0) {
+          const int mm = (t < NTL && t <= E - rw) ? min(t - 1, E - 1 - rw) : 0;
+          const int mw = min(min(NTL, 32 * (r + 1)) - 2, E - 1 - rw);  // max of mm over the warp
+          const double2 *F = hb + rw * NTL + 1;                        // F_r[m] = F[m]
+          int m = m0 + warp;
+          const double2 *qd = Q + (rw + m + 1) * NTL + t - m - 1;       // q_{r+m+1}[t-m-1]
+          for (; m <= mw; m += 4 * NW, qd += 4 * NW * (NTL - 1)) {     // warp-uniform bound
+            if (m <= mm) a0 = cfma(F[m], qd[0], a0);
+            if (m + NW <= mm) a1 = cfma(F[m + NW], qd[NW * (NTL - 1)], a1);
+            if (m + 2 * NW <= mm) a2 = cfma(F[m + 2 * NW], qd[2 * NW * (NTL - 1)], a2);
+            if (m + 3 * NW <= mm) a3 = cfma(F[m + 3 * NW], qd[3 * NW * (NTL - 1)], a3);
+          }
+        }
+        if (t < NTL) pw[sl * NTL + t] = cadd(cadd(a0, a2), cadd(a1, a3));
+      }
+    }
+    if (warp == 0) {
+      const double2 *pp = part + (((b + 1) & 1) * NW) * 2 * NTL;  // written in block b-1
+      double2 u1[NRT], u2[NRT], u3[NRT];
+      // row j
+      {
+        const double2 h = hb[j * NTL + 1];
+        const double2 f1 = (E - 1 - j >= 1 && NTL > 2) ? hb[j * NTL + 2] : c0();
+        shift_up<NRT>(qa, 1, lane, u1);
+        shift_up<NRT>(qb, 2, lane, u2);
+#pragma unroll
+        for (int r = 0; r < NRT; ++r) {
+          const int t = lane + 32 * r;
+          double2 q = cfms(h, u1[r], qa[r]);
+          q = cfms(f1, u2[r], q);
+          if (t < NTL) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) q = csub(q, pp[w * 2 * NTL + t]);
+          }
+          if (t > E - j) q = c0();  // above the degree of q_j
+          qb[r] = q;                // (qb <- q_j, qa stays q_{j+1} for row j-1)
+          if (t < NTL) Q[j * NTL + t] = q;
+        }
+      }
+      // row j-1: q_{j+1} = qa, q_j = qb, q_{j+2} = u2 shifted by 2 (recompute by 3)
+      if (j >= 1) {
+        const int i = j - 1;
+        const double2 h = hb[i * NTL + 1];
+        const double2 f1 = (NTL > 2) ? hb[i * NTL + 2] : c0();  // (E-1-i >= 1)
+        const double2 f2 = (E - 1 - i >= 2 && NTL > 3) ? hb[i * NTL + 3] : c0();
+        double2 s1[NRT];
+        shift_up<NRT>(qb, 1, lane, s1);  // q_j[t-1]
+        shift_up<NRT>(qa, 2, lane, u1);  // q_{j+1}[t-2]
+        // q_{j+2}[t-3] = u2 (q_{j+2}[t-2]) shifted by one more
+        shift_up<NRT>(u2, 1, lane, u3);
+#pragma unroll
+        for (int r = 0; r < NRT; ++r) {
+          const int t = lane + 32 * r;
+          double2 q = cfms(h, s1[r], qb[r]);
+          q = cfms(f1, u1[r], q);
+          q = cfms(f2, u3[r], q);
+          if (t < NTL) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) q = csub(q, pp[w * 2 * NTL + NTL + t]);
+          }
+          if (t > E - i) q = c0();
+          qa[r] = q;  // q_{j-1}: the next block's q_{j'+1}; qb = q_j its q_{j'+2}
+          if (t < NTL) Q[i * NTL + t] = q;
+        }
       }
     }
     team_sync<NW, TEAMS>(team);
@@ -565,16 +680,17 @@ __device__ __forceinline__ void reduce_phased(double2 (&A)[CS], int &label, doub
 }
 
 // ================================================================ one term, one team
-// g(t) of one term (valid in warp 0 of the team); sign and weight from the decode (warp 0).
-// CMP: keep the live columns contiguous (compaction) and skip finished slot groups.
+// a4-a6 of one term: decode, build, Hessenberg reduction into the band T.hb; sign and weight
+// from the decode (warp 0).  Ends without a barrier after the last band writes.
+// CMP: phased reduction (compaction of the live columns).
 template <int S, int CS, int NW, int TEAMS, bool CMP>
-__device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J, uint64_t t,
-                             const TeamMem &T, int tid, int team, int &sign, double &weight) {
+__device__ __forceinline__ void team_reduce(const PatDesc &P, const Pattern &D, const JobDev &J,
+                                            uint64_t t, const TeamMem &T, int tid, int team,
+                                            int &sign, double &weight) {
   using Sh = Shape<S, CS, NW>;
   constexpr int RC = Sh::RC, CC = Sh::CC;
   const int lane = tid & 31, warp = tid >> 5;
-  const int H = D.H, n = D.n, E = D.E, o = D.o, NTL = D.NTL;
-  const bool loops = D.loops;
+  const int H = D.H, E = D.E, o = D.o, NTL = D.NTL;
   double2 *hb = T.hb;
 
 #ifdef LHAF_PHASE_TIMING
@@ -723,7 +839,20 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
   if (E >= 2 && par == 0 && label < E - 1 && E - label < NTL)
     hb[label * NTL + E - label] = cmul(hb[label * NTL + E - label], *betap);
   LHAF_PHASE(1)
+}
 
+// g(t) of one term (valid in warp 0 of the team); sign and weight from the decode (warp 0).
+template <int S, int CS, int NW, int TEAMS, bool CMP>
+__device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J, uint64_t t,
+                             const TeamMem &T, int tid, int team, int &sign, double &weight) {
+  team_reduce<S, CS, NW, TEAMS, CMP>(P, D, J, t, T, tid, team, sign, weight);
+#ifdef LHAF_PHASE_TIMING
+  long long t_last_ = clock64();
+#endif
+  const int lane = tid & 31, warp = tid >> 5;
+  const int n = D.n, E = D.E, NTL = D.NTL;
+  const bool loops = D.loops;
+  const double2 *hb = T.hb;
   double2 g = c0();
   double2 *Q = T.u1;  // [E+1][NTL]: Q[j][t] = coefficient of x^{deg q_j - t}
   {
@@ -732,7 +861,8 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
       if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
       else labudde<2>(hb, Q, E, NTL, lane);
     } else {
-      if (NTL <= 32) labudde_team<1, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
+      // (two rows per barrier pays at NTL <= 32; one row per barrier above, measured)
+      if (NTL <= 32) labudde_team2<1, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
       else labudde_team<2, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
     }
   }
@@ -806,6 +936,140 @@ sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
   }
 }
 
+// ================================================================ v4: reduction teams + tail warp
+// La Budde + series of one term in one warp (a7-a9) from a band hb written by a team; Q and
+// the series scratch are the warp's own.
+__device__ __forceinline__ double2 warp_tail(const double2 *hb, double2 *Q, const Pattern &D,
+                                             int lane) {
+  const int n = D.n, E = D.E, NTL = D.NTL;
+#ifdef LHAF_V4_NOTAIL  // diagnostic: the reduction teams' throughput alone
+  return c0();
+#endif
+  if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
+  else labudde<2>(hb, Q, E, NTL, lane);
+  const double2 *cB = Q;
+  const double2 *cM = D.loops ? Q + NTL : Q;
+  double2 *scr = Q + (E + 1) * NTL;
+  if (n + 2 <= 32) return series<1>(cM, cB, n, NTL, D.loops, scr, lane);
+  if (n + 2 <= 64) return series<2>(cM, cB, n, NTL, D.loops, scr, lane);
+  return series<5>(cM, cB, n, NTL, D.loops, scr, lane);
+}
+
+__device__ __forceinline__ void nb_sync(int id, int cnt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+
+// Two reduction teams and one tail warpgroup per CTA (NW = 4).  Team t reduces the unit's
+// terms tb+t, tb+t+2, ... into its two band buffers in turn; tail warp t takes team t's bands
+// in order (single-warp La Budde, series, accumulation) while the team reduces the next term,
+// so the reduction is the only work on the teams' critical path.  setmaxnreg moves registers
+// from the tail warpgroup (RA) to the reduction warpgroups (RT): the launch gives every warp
+// 168 (3 warps per SM sub-partition) and 2 RT + RA <= 3 * 168.  Named barriers hand a buffer
+// over: FULL(t, b) = 3 + 2t + b (team arrives, tail warp syncs), EMPTY(t, b) = 7 + 2t + b
+// (tail warp arrives, team syncs before refilling b); 1 and 2 are the teams' own, 12 brackets
+// the unit fetch, 13 joins the two tail warps' sums.
+template <int S, int CS, int RT, int RA, bool CMP>
+__global__ void __launch_bounds__(384, 1)
+sieve_v4(JobDev J, uint64_t ubeg, uint64_t uend, int team_words, int aux_words) {
+  constexpr int NW = 4;
+  using Sh = Shape<S, CS, NW>;
+  static_assert(2 * RT + RA <= 3 * 168, "register budget");
+  extern __shared__ double2 smem[];
+  __shared__ unsigned long long s_unit;
+  __shared__ double2 s_hand[2][2];  // (sign * weight, weight) per team and buffer
+  __shared__ double s_acc[6];
+  constexpr int TS = 32 * NW, NT = 3 * TS, HAND = TS + 32;
+  const int wg = threadIdx.x / TS, tid = threadIdx.x % TS;
+  const int warp = tid >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 2 * team_words + aux_words; i += NT) smem[i] = c0();
+  double2 *abase = smem + 2 * (size_t)team_words;
+  // the two roles run separate loops (so that each is compiled under its own register budget);
+  // barrier 12 (whole CTA) brackets the unit fetch
+  if (wg < 2) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(RT));
+    const int team = wg;
+    double2 *base = smem + (size_t)team * team_words;
+    for (;;) {
+      nb_sync(12, NT);
+      if (threadIdx.x == 0) s_unit = ubeg + atomicAdd(J.counter, 1ull);
+      nb_sync(12, NT);
+      const uint64_t u = s_unit;
+      if (u >= uend) break;
+      const PatDesc P = J.descs[find_pattern(J, u)];
+      const Pattern D = pattern_of(P);
+      const uint64_t tb = (u - P.unit_begin) * P.chunk;
+      const uint64_t te = min(tb + P.chunk, P.T_eval);
+      const int EN = D.E * D.NTL;
+      TeamMem T;
+      T.u1 = base + 2 * EN;
+      T.wv = reinterpret_cast<int *>(T.u1 + Sh::red_words());
+      T.ww = reinterpret_cast<double *>(T.u1 + Sh::red_words() + 32);
+      int use = 0;
+      for (uint64_t t = tb + team; t < te; t += 2, ++use) {
+        const int b = use & 1;
+        if (use >= 2) nb_sync(7 + 2 * team + b, HAND);
+        T.hb = base + b * EN;
+        int sign = 1;
+        double weight = 1.0;
+#ifndef LHAF_V4_NOTEAM  // diagnostic: the tail warps' throughput alone (bands of zeros)
+        team_reduce<S, CS, NW, 2, CMP>(P, D, J, t, T, tid, team, sign, weight);
+#endif
+        if (tid == 0) s_hand[team][b] = make_double2(sign * weight, weight);
+        nb_arrive(3 + 2 * team + b, HAND);
+      }
+    }
+  } else {
+    // tail warps 0 and 1 serve teams 0 and 1 (single-warp La Budde + series, in term order);
+    // warps 2 and 3 only keep the unit barrier
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(RA));
+    for (;;) {
+      nb_sync(12, NT);
+      nb_sync(12, NT);
+      const uint64_t u = s_unit;
+      if (u >= uend) break;
+      if (warp >= 2) continue;
+      const PatDesc P = J.descs[find_pattern(J, u)];
+      const Pattern D = pattern_of(P);
+      const uint64_t tb = (u - P.unit_begin) * P.chunk;
+      const uint64_t te = min(tb + P.chunk, P.T_eval);
+      const int nterm = (int)(te - tb);
+      const int EN = D.E * D.NTL;
+      const int team = warp, nt = (nterm - team + 1) / 2;
+      double2 *Q = abase + (size_t)team * (aux_words / 2);
+      double rh = 0, rl = 0, ih = 0, il = 0, ah = 0, al = 0;
+      for (int use = 0; use < nt; ++use) {
+        const int b = use & 1;
+        nb_sync(3 + 2 * team + b, HAND);
+        const double2 g = warp_tail(smem + (size_t)team * team_words + b * EN, Q, D, lane);
+        const double2 hw = s_hand[team][b];
+        __syncwarp();
+        if (use + 2 < nt) nb_arrive(7 + 2 * team + b, HAND);
+        if (lane == 0) {
+          dd_add(rh, rl, hw.x * g.x);
+          dd_add(ih, il, hw.x * g.y);
+          dd_add(ah, al, hw.y * hypot(g.x, g.y));
+        }
+      }
+      if (team == 1 && lane == 0) {
+        s_acc[0] = rh; s_acc[1] = rl; s_acc[2] = ih; s_acc[3] = il; s_acc[4] = ah; s_acc[5] = al;
+      }
+      nb_sync(13, 64);
+      if (team == 0 && lane == 0) {
+        dd_add_dd(rh, rl, s_acc[0], s_acc[1]);
+        dd_add_dd(ih, il, s_acc[2], s_acc[3]);
+        dd_add_dd(ah, al, s_acc[4], s_acc[5]);
+        Partial q;
+        q.re_hi = rh; q.re_lo = rl; q.im_hi = ih; q.im_lo = il; q.abs_hi = ah; q.abs_lo = al;
+        q.pad0 = 0; q.pad1 = 0;
+        J.partials[u] = q;
+      }
+    }
+  }
+}
+
 // g(t) (unweighted) of pattern 0 for a list of term indices; one team per index.
 template <int S, int CS, int NW, int TEAMS, int REGS, bool CMP>
 __global__ void __maxnreg__(REGS)
@@ -871,6 +1135,42 @@ struct Inst {
   }
 };
 
+template <int S, int CS, int RT, int RA, bool CMP>
+struct Inst4 {
+  static constexpr int NW = 4;
+  using Sh = Shape<S, CS, NW>;
+  static constexpr int EMAX = Sh::EMAX;
+  static constexpr int THREADS = 3 * 32 * NW;
+  static cudaError_t sieve(const JobDev &job, int E, int NTL, int n, uint64_t ubeg, uint64_t uend,
+                           int num_sms, cudaStream_t s) {
+    const int tw = 2 * E * NTL + Sh::red_words() + 64;
+    const int aw = 2 * ((E + 1) * NTL + 3 * (n + 2));
+    const size_t smem = (size_t)(2 * tw + aw) * sizeof(double2);
+    auto *kern = sieve_v4<S, CS, RT, RA, CMP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (getenv("LHAF_DEBUG_V4")) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, kern);
+      fprintf(stderr, "v4: E=%d NTL=%d smem=%zu per_sm=%d regs=%d maxthreads=%d\n", E, NTL, smem, per_sm,
+              fa.numRegs, fa.maxThreadsPerBlock);
+    }
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t units = uend - ubeg;
+    uint64_t grid = (uint64_t)num_sms * per_sm;
+    if (grid > units) grid = units;
+    e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw, aw);
+    return cudaGetLastError();
+  }
+};
+
 // <S, CS, NW, TEAMS, registers per thread>.  Each SM sub-partition has 16K registers, so a
 // warp of R registers allows floor(512 / R) warps per sub-partition.
 using I9 = Inst<1, 9, 1, 4, 128>;
@@ -891,6 +1191,13 @@ using P62 = Inst<2, 31, 4, 1, 255>;
 // (LHAF_V3_ALT=5) phased reduction at 255 registers
 using R48 = Inst<2, 24, 3, 1, 255, true>;
 using R62 = Inst<2, 31, 4, 1, 255, true>;
+// (LHAF_V3_ALT=6) single-phase reduction at 168 registers: 3 CTAs / SM for E <= 62
+using T62 = Inst<2, 31, 4, 1, 168>;
+// (LHAF_V3_ALT=8) v4: two reduction teams + one tail warp per CTA
+using V62 = Inst4<2, 31, 232, 40, false>;
+using W62 = Inst4<2, 31, 224, 56, false>;
+using X62 = Inst4<2, 31, 216, 72, false>;
+using Y62 = Inst4<2, 31, 208, 88, false>;
 static int alt_mode() {
   static const int m = [] { const char *e = getenv("LHAF_V3_ALT"); return e ? atoi(e) : 0; }();
   return m;
@@ -925,6 +1232,7 @@ extern "C" int lhaf_debug_phase_cycles(unsigned long long *out8) {
     if (E > 32 && E <= v3::P48::EMAX) return v3::P48::CALL; \
     if (E > 48 && E <= v3::P62::EMAX) return v3::P62::CALL; \
   }                                             \
+  if (v3::alt_mode() == 6 && E > 48 && E <= v3::T62::EMAX) return v3::T62::CALL; \
   if (v3::alt_mode() == 5) {                    \
     if (E > 32 && E <= v3::R48::EMAX) return v3::R48::CALL; \
     if (E > 48 && E <= v3::R62::EMAX) return v3::R62::CALL; \
@@ -949,6 +1257,14 @@ cudaError_t launch_sieve_v3(const JobDev &job, int e_max, int ntl_max, int n_max
   cudaError_t e = v3::ensure_inv();
   if (e != cudaSuccess) return e;
   const int E = e_max;
+  if (v3::alt_mode() == 8 && E > 48 && E <= v3::V62::EMAX)
+    return v3::V62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
+  if (v3::alt_mode() == 9 && E > 48 && E <= v3::W62::EMAX)
+    return v3::W62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
+  if (v3::alt_mode() == 10 && E > 48 && E <= v3::X62::EMAX)
+    return v3::X62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
+  if (v3::alt_mode() == 11 && E > 48 && E <= v3::Y62::EMAX)
+    return v3::Y62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
   LHAF_V3_DISPATCH(sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s))
 }
 
