@@ -155,7 +155,7 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(cfg, reps, seconds_target=15.0):
+def cpu_baseline_sample(cfg, reps, seconds_target=22.0):
     import oracle
     r0 = reps[0] if reps.ndim == 2 else reps
     nthreads = oracle.num_threads()
