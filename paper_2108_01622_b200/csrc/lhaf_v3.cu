@@ -1182,8 +1182,8 @@ using I62 = Inst<2, 31, 4, 1, 232, true>;  // 2 CTAs / SM (2 warps per 16K-regis
 using I64 = Inst<2, 32, 4, 1, 168, true>;
 // alternatives (LHAF_V3_ALT=1): more lanes per row, fewer registers, more warps per SM
 using A26 = Inst<2, 13, 2, 2, 104>;   // E <= 26: 4 warps / CTA
-using A48 = Inst<4, 12, 6, 1, 104>;   // E <= 48: 6 warps / CTA
-using A64 = Inst<4, 16, 8, 1, 128>;   // E <= 64: 8 warps / CTA
+using A48 = Inst<4, 12, 6, 1, 128, true>;   // E <= 48: 6 warps / CTA
+using A64 = Inst<4, 16, 8, 1, 128, true>;   // E <= 64: 8 warps / CTA
 // (LHAF_V3_ALT=3) single-phase reduction (no compaction)
 using P25 = Inst<1, 25, 1, 4, 168>;
 using P48 = Inst<2, 24, 3, 1, 168>;
