@@ -150,3 +150,28 @@ def random_pattern(k: int, N: int, rng: np.random.Generator, max_rep: int | None
             reps[i] += 1
             placed += 1
     return reps
+
+
+def gaussian_state(U: np.ndarray, r, eta=1.0, beta=None, nbar=None):
+    """Covariance sigma (2m x 2m) and mean alpha (2m) in the (a_1..a_m, a_1^dag..a_m^dag) basis
+    (sigma_ij = <a_i a_j^dag + a_j^dag a_i>/2 - alpha_i alpha_j^*) of: single-mode
+    squeezed (r_i) or thermal (nbar_i) inputs, per-mode transmission eta_i (pure loss), the
+    interferometer U (a -> U a), then a displacement beta (<a> = beta).  Input construction for
+    tests (the probability formula itself is the method)."""
+    m = U.shape[0]
+    r = np.broadcast_to(np.asarray(r, float), (m,))
+    eta = np.broadcast_to(np.asarray(eta, float), (m,))
+    ch, sh = np.cosh(r), np.sinh(r)
+    sig = np.zeros((2 * m, 2 * m), complex)
+    for i in range(m):
+        sig[i, i] = sig[i + m, i + m] = sh[i] ** 2 + 0.5
+        sig[i, i + m] = sig[i + m, i] = -ch[i] * sh[i]
+    if nbar is not None:
+        sig = sig + np.diag(np.concatenate([nbar, nbar]).astype(complex))
+    e2 = np.concatenate([eta, eta])
+    sig = np.sqrt(e2)[:, None] * sig * np.sqrt(e2)[None, :] + np.diag((1.0 - e2) / 2.0)
+    S = np.block([[U, np.zeros((m, m))], [np.zeros((m, m)), U.conj()]])
+    sig = S @ sig @ S.conj().T
+    b = np.zeros(m, complex) if beta is None else np.asarray(beta, complex)
+    alpha = np.concatenate([b, b.conj()])
+    return sig, alpha

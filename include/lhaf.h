@@ -120,6 +120,31 @@ lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t
 lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
                             int32_t k, int32_t mode, int32_t n_cut, double *out);
 
+/* Photon-number pattern probabilities of an M-mode Gaussian state (App. A,
+ * P:301-320, Eq. (mixed_prob)):
+ *   P(n | sigma, alpha) = exp(-alpha^dag sigma_Q^{-1} alpha / 2) / (sqrt(det sigma_Q) prod_i n_i!)
+ *                         * lhaf(A_n),
+ * sigma_Q = sigma + I/2, A = X (I - sigma_Q^{-1}), gamma = alpha^dag sigma_Q^{-1}; A_n and
+ * gamma_n repeat indices i and i+M n_i times (lhaf_rpt_mixed, natural pairing).
+ * sigma: 2M*2M c128 in the basis (a_1..a_M, a_1^dag..a_M^dag),
+ *   sigma_ij = <a_i a_j^dag + a_j^dag a_i>/2 - alpha_i alpha_j^* (P:303-305);
+ * alpha: 2M c128, alpha_i = <a_i> (so alpha_{i+M} = conj(alpha_i)); n: M int32 >= 0.
+ * pure != 0: the caller asserts the state is pure, so A = B (+) B* and the probability is
+ *   prefactor |lhaf(B_n)|^2 / prod n_i! with B = A[0:M, 0:M] and loops gamma[0:M],
+ *   a loop hafnian of half the size (lhaf_rpt).
+ * out[0] = P, out[1] = the imaginary residue of the evaluated expression (0 up to rounding).
+ * sigma_Q is inverted on the host (LU with partial pivoting, one per call); the loop hafnian
+ * runs on the device.  Errors: LHAF_E_ARG (null pointer, M < 1 or > 2048, n_i < 0, sigma_Q
+ * singular or det(sigma_Q) <= 0), otherwise as lhaf_rpt / lhaf_rpt_mixed. */
+lhaf_status lhaf_gbs_prob(const double *sigma, const double *alpha, int32_t M, const int32_t *n,
+                          int32_t pure, double out[2]);
+
+/* The ingredients of lhaf_gbs_prob without a device: A (2M*2M c128), gamma (2M c128) and the
+ * prefactor exp(-alpha^dag sigma_Q^{-1} alpha / 2) / sqrt(det sigma_Q) (out_pref: re, im).
+ * Caller-owned outputs, written only on LHAF_OK.  Errors as lhaf_gbs_prob. */
+lhaf_status lhaf_gbs_matrices(const double *sigma, const double *alpha, int32_t M, double *A,
+                              double *gamma, double out_pref[2]);
+
 /* Same three entry points with DEVICE pointers for A / gamma / out (reps stays on the host,
  * since planning is host integer work) and an explicit cudaStream_t (passed as void*; NULL =
  * the legacy default stream).  The call is asynchronous with respect to the host only in the

@@ -16,6 +16,8 @@ Parity status per function:
   matched_reps      pinned: the paper's worked example n = (2,1,0,3) -> 6 terms
   fds_term          pinned: 2x2 closed form; full-sum agreement with lhaf_brute/lhaf_et
   lhaf_fds          pinned: agreement with lhaf_brute / lhaf_et, closed forms
+  gbs_prob          pinned: squeezed-vacuum, coherent (Poisson) and thermal (geometric)
+                    photon statistics, the sum rule sum_n P(n) = 1   (tests/test_gbs_pins.py)
 """
 from __future__ import annotations
 
@@ -250,3 +252,28 @@ def fds_range(A, gamma, reps, t0: int, t1: int, mixed: bool = False):
 def num_threads() -> int:
     fds_range(np.zeros((1, 1)), np.zeros(1), [0], 0, 0)
     return int(_load().orc_num_threads())
+
+
+def gbs_prob(sigma, alpha, n) -> complex:
+    """P(n | sigma, alpha) of a Gaussian state, App. A step by step:
+    sigma_Q = sigma + I/2 (P:307), O = I - sigma_Q^{-1}, A = X O, gamma = alpha^dag sigma_Q^{-1}
+    (P:308-312); A_n by repeating rows/cols i and i+M n_i times, its diagonal replaced by the
+    repeated gamma; P = exp(-alpha^dag sigma_Q^{-1} alpha / 2) / (sqrt(det sigma_Q)
+    prod n_i!) lhaf(A_n) (Eq. mixed_prob) with lhaf by brute force (<= 16 indices, else
+    the ET tier)."""
+    import math
+    sigma = np.asarray(sigma, complex)
+    alpha = np.asarray(alpha, complex)
+    M = alpha.shape[0] // 2
+    sq = sigma + 0.5 * np.eye(2 * M)
+    qi = np.linalg.inv(sq)
+    O = np.eye(2 * M) - qi
+    X = np.block([[np.zeros((M, M)), np.eye(M)], [np.eye(M), np.zeros((M, M))]])
+    A = X @ O
+    gamma = alpha.conj() @ qi
+    idx = [i for i in range(M) for _ in range(n[i])] + [i + M for i in range(M) for _ in range(n[i])]
+    An = A[np.ix_(idx, idx)].copy()
+    np.fill_diagonal(An, gamma[idx])
+    lh = (lhaf_brute(An) if len(idx) <= 16 else lhaf_et(An)) if idx else 1.0
+    pref = np.exp(-0.5 * (alpha.conj() @ qi @ alpha)) / np.sqrt(np.linalg.det(sq))
+    return complex(pref * lh / np.prod([math.factorial(int(k)) for k in n]))

@@ -6,7 +6,8 @@ in the library's CUDA kernels.  There is no CPU fallback: if liblhaf.so is missi
 the binding raises, and without a CUDA device every compute call raises ``LhafError``.
 
 Names follow the C-ABI: ``lhaf_rpt``, ``lhaf_rpt_batch``, ``lhaf_rpt_mixed``,
-``lhaf_rpt_batch_dev``, ``lhaf_plan``, ``lhaf_decode``, the ``Job`` wrapper over
+``lhaf_rpt_batch_dev``, ``lhaf_rpt_cutoff``, ``lhaf_gbs_matrices``, ``lhaf_gbs_prob``,
+``lhaf_plan``, ``lhaf_decode``, the ``Job`` wrapper over
 ``lhaf_job_*``, and the rank calls ``lhaf_get_unique_id`` / ``lhaf_init_rank``.
 """
 from __future__ import annotations
@@ -68,6 +69,8 @@ def _load() -> ctypes.CDLL:
         "lhaf_rpt_batch": ([dp, dp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32, dp]),
         "lhaf_rpt_mixed": ([dp, dp, ip, ctypes.c_int32, dp]),
         "lhaf_rpt_cutoff": ([dp, dp, ip, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, dp]),
+        "lhaf_gbs_matrices": ([dp, dp, ctypes.c_int32, dp, dp, dp]),
+        "lhaf_gbs_prob": ([dp, dp, ctypes.c_int32, ip, ctypes.c_int32, dp]),
         "lhaf_rpt_batch_dev": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
                                 ctypes.c_int32, vp, vp]),
         "lhaf_job_create": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
@@ -125,6 +128,7 @@ def reload_library():
 
 # every symbol include/lhaf.h declares (checked by tests/test_capi.py)
 EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed", "lhaf_rpt_cutoff",
+            "lhaf_gbs_matrices", "lhaf_gbs_prob",
             "lhaf_rpt_batch_dev", "lhaf_job_create", "lhaf_job_info_get", "lhaf_job_reset",
             "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_finalize", "lhaf_job_abs_sum",
             "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
@@ -195,6 +199,27 @@ def lhaf_rpt_mixed(A2, gamma2, reps) -> complex:
     A2, gamma2, reps = _c128(A2), _c128(gamma2), _i32(reps)
     out = np.zeros(2)
     _check(_lib.lhaf_rpt_mixed(_dp(A2), _dp(gamma2), _ip(reps), reps.shape[0], _dp(out)))
+    return complex(out[0], out[1])
+
+
+def lhaf_gbs_matrices(sigma, alpha):
+    """(A, gamma, prefactor) of a Gaussian state (App. A): A = X (I - sigma_Q^-1),
+    gamma = alpha^dag sigma_Q^-1, prefactor exp(-alpha^dag sigma_Q^-1 alpha / 2) / sqrt(det sigma_Q)."""
+    sigma, alpha = _c128(sigma), _c128(alpha)
+    M = alpha.shape[0] // 2
+    A = np.zeros((2 * M, 2 * M), np.complex128)
+    g = np.zeros(2 * M, np.complex128)
+    pref = np.zeros(2)
+    _check(_lib.lhaf_gbs_matrices(_dp(sigma), _dp(alpha), M, _dp(A), _dp(g), _dp(pref)))
+    return A, g, complex(pref[0], pref[1])
+
+
+def lhaf_gbs_prob(sigma, alpha, n, pure: bool = False) -> complex:
+    """P(n | sigma, alpha) (Eq. mixed_prob, P:317); pure=True uses |lhaf(B_n)|^2 (P:322-334).
+    Returns a complex number whose imaginary part is the rounding residue."""
+    sigma, alpha, n = _c128(sigma), _c128(alpha), _i32(n)
+    out = np.zeros(2)
+    _check(_lib.lhaf_gbs_prob(_dp(sigma), _dp(alpha), n.shape[0], _ip(n), 1 if pure else 0, _dp(out)))
     return complex(out[0], out[1])
 
 

@@ -211,6 +211,11 @@ uint64_t chunk_for(uint64_t T_eval) {
 
 }  // namespace
 
+int lhaf::set_error(int status, const char *msg) {
+  g_err = msg;
+  return status;
+}
+
 // ------------------------------------------------------------------ job
 struct lhaf_job {
   int batch = 0, kdim = 0, d_max = 0, n_max = 0, variant = 1;

@@ -76,4 +76,7 @@ cudaError_t launch_terms_v3(const JobDev &job, int e_max, int ntl_max, int n_max
                             int nt, double2 *g_out, cudaStream_t s);
 double v3_flops_per_term(int d, int n, bool loops);
 
+// sets lhaf_last_error() for entry points outside lhaf_host.cpp (returns its status argument)
+int set_error(int status, const char *msg);
+
 }  // namespace lhaf
