@@ -145,6 +145,16 @@ lhaf_status lhaf_gbs_prob(const double *sigma, const double *alpha, int32_t M, c
 lhaf_status lhaf_gbs_matrices(const double *sigma, const double *alpha, int32_t M, double *A,
                               double *gamma, double out_pref[2]);
 
+/* Proposal probability of the MIS importance sampler: singles Poisson(|alpha_j|^2)
+ * and photon pairs Poisson(|B_jk|^2) (j < k; 1/2 |B_jj|^2 for j = k) combined into a pattern:
+ *   Q(n | B, alpha) = exp(-sum_j |alpha_j|^2 - 1/2 sum_{j,k} |B_jk|^2) / prod_i n_i! lhaf(C_n),
+ * C_n = |B_n|^2 elementwise with its diagonal replaced by |alpha_n|^2 -- a loop hafnian of a
+ * non-negative matrix, evaluated by the same device path (lhaf_rpt with A = |B|^2, gamma =
+ * |alpha|^2).  B: M*M c128 (symmetric), alpha: M c128, n: M int32.  out[0] = Q, out[1] = the
+ * imaginary residue (0).  Errors as lhaf_rpt, plus LHAF_E_ARG for M < 1 or n_i < 0. */
+lhaf_status lhaf_ips_prob(const double *B, const double *alpha, int32_t M, const int32_t *n,
+                          double out[2]);
+
 /* Same three entry points with DEVICE pointers for A / gamma / out (reps stays on the host,
  * since planning is host integer work) and an explicit cudaStream_t (passed as void*; NULL =
  * the legacy default stream).  The call is asynchronous with respect to the host only in the

@@ -18,6 +18,7 @@ Parity status per function:
   lhaf_fds          pinned: agreement with lhaf_brute / lhaf_et, closed forms
   gbs_prob          pinned: squeezed-vacuum, coherent (Poisson) and thermal (geometric)
                     photon statistics, the sum rule sum_n P(n) = 1   (tests/test_gbs_pins.py)
+  ips_prob          pinned: single-mode Poisson convolution closed form, sum rule
 """
 from __future__ import annotations
 
@@ -277,3 +278,19 @@ def gbs_prob(sigma, alpha, n) -> complex:
     lh = (lhaf_brute(An) if len(idx) <= 16 else lhaf_et(An)) if idx else 1.0
     pref = np.exp(-0.5 * (alpha.conj() @ qi @ alpha)) / np.sqrt(np.linalg.det(sq))
     return complex(pref * lh / np.prod([math.factorial(int(k)) for k in n]))
+
+
+def ips_prob(B, alpha, n) -> float:
+    """MIS proposal probability: Q(n) = exp(-sum |alpha_j|^2 - sum_{j,k} |B_jk|^2 / 2)
+    / prod n_i! lhaf(C_n), C_n = |B_n|^2 with its diagonal replaced by |alpha_n|^2, formed
+    explicitly (B_n repeats row/col i n_i times) and summed by brute force / ET."""
+    import math
+    B = np.asarray(B, complex)
+    alpha = np.asarray(alpha, complex)
+    M = alpha.shape[0]
+    idx = [i for i in range(M) for _ in range(n[i])]
+    Cn = np.abs(B[np.ix_(idx, idx)]) ** 2 + 0j
+    np.fill_diagonal(Cn, np.abs(alpha[idx]) ** 2)
+    lh = (lhaf_brute(Cn) if len(idx) <= 16 else lhaf_et(Cn)) if idx else 1.0
+    pref = math.exp(-np.sum(np.abs(alpha) ** 2) - 0.5 * np.sum(np.abs(B) ** 2))
+    return float((pref * lh).real / np.prod([math.factorial(int(k)) for k in n]))

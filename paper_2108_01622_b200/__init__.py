@@ -7,6 +7,7 @@ the binding raises, and without a CUDA device every compute call raises ``LhafEr
 
 Names follow the C-ABI: ``lhaf_rpt``, ``lhaf_rpt_batch``, ``lhaf_rpt_mixed``,
 ``lhaf_rpt_batch_dev``, ``lhaf_rpt_cutoff``, ``lhaf_gbs_matrices``, ``lhaf_gbs_prob``,
+``lhaf_ips_prob``,
 ``lhaf_plan``, ``lhaf_decode``, the ``Job`` wrapper over
 ``lhaf_job_*``, and the rank calls ``lhaf_get_unique_id`` / ``lhaf_init_rank``.
 """
@@ -71,6 +72,7 @@ def _load() -> ctypes.CDLL:
         "lhaf_rpt_cutoff": ([dp, dp, ip, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, dp]),
         "lhaf_gbs_matrices": ([dp, dp, ctypes.c_int32, dp, dp, dp]),
         "lhaf_gbs_prob": ([dp, dp, ctypes.c_int32, ip, ctypes.c_int32, dp]),
+        "lhaf_ips_prob": ([dp, dp, ctypes.c_int32, ip, dp]),
         "lhaf_rpt_batch_dev": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
                                 ctypes.c_int32, vp, vp]),
         "lhaf_job_create": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
@@ -128,7 +130,7 @@ def reload_library():
 
 # every symbol include/lhaf.h declares (checked by tests/test_capi.py)
 EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed", "lhaf_rpt_cutoff",
-            "lhaf_gbs_matrices", "lhaf_gbs_prob",
+            "lhaf_gbs_matrices", "lhaf_gbs_prob", "lhaf_ips_prob",
             "lhaf_rpt_batch_dev", "lhaf_job_create", "lhaf_job_info_get", "lhaf_job_reset",
             "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_finalize", "lhaf_job_abs_sum",
             "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
@@ -221,6 +223,14 @@ def lhaf_gbs_prob(sigma, alpha, n, pure: bool = False) -> complex:
     out = np.zeros(2)
     _check(_lib.lhaf_gbs_prob(_dp(sigma), _dp(alpha), n.shape[0], _ip(n), 1 if pure else 0, _dp(out)))
     return complex(out[0], out[1])
+
+
+def lhaf_ips_prob(B, alpha, n) -> float:
+    """MIS proposal probability Q(n | B, alpha)."""
+    B, alpha, n = _c128(B), _c128(alpha), _i32(n)
+    out = np.zeros(2)
+    _check(_lib.lhaf_ips_prob(_dp(B), _dp(alpha), n.shape[0], _ip(n), _dp(out)))
+    return float(out[0])
 
 
 def lhaf_rpt_cutoff(A, gamma, reps_fixed, mode: int, n_cut: int) -> np.ndarray:

@@ -1,6 +1,6 @@
 // lhaf_gbs.cpp -- photon-number probabilities of Gaussian states on top of the loop hafnian
 // (App. A of the paper, Eq. (mixed_prob); pure block form
-// P:322-334).  Host arithmetic on the 2M x 2M covariance (one LU per state: sigma_Q^{-1} and
+// P:322-334), and the MIS proposal probability Q(n | B, alpha).  Host arithmetic on the 2M x 2M covariance (one LU per state: sigma_Q^{-1} and
 // det sigma_Q), then ONE device loop hafnian through the C-ABI (lhaf_rpt_mixed, or lhaf_rpt on
 // the half-size B_n for pure states).  Product code: shares nothing with oracle/.
 #include <cmath>
@@ -154,6 +154,35 @@ lhaf_status lhaf_gbs_prob(const double *sigma, const double *alpha, int32_t M, c
   const cd p = pref * val / fact;
   out[0] = p.real();
   out[1] = p.imag();
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_ips_prob(const double *B, const double *alpha, int32_t M, const int32_t *n,
+                          double out[2]) {
+  if (!B || !alpha || !n || !out) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "null pointer");
+  if (M < 1 || M > 4096) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "bad mode count");
+  double fact = 1.0, expo = 0.0;
+  for (int i = 0; i < M; ++i) {
+    if (n[i] < 0) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "negative photon count");
+    for (int c = 2; c <= n[i]; ++c) fact *= (double)c;
+  }
+  // C = |B|^2 elementwise (its diagonal: the within-mode pair weight), loops |alpha|^2
+  std::vector<double> C((size_t)2 * M * M, 0.0), g((size_t)2 * M, 0.0);
+  for (size_t i = 0; i < (size_t)M * M; ++i) {
+    const double a = B[2 * i] * B[2 * i] + B[2 * i + 1] * B[2 * i + 1];
+    C[2 * i] = a;
+    expo += 0.5 * a;
+  }
+  for (int i = 0; i < M; ++i) {
+    const double a = alpha[2 * i] * alpha[2 * i] + alpha[2 * i + 1] * alpha[2 * i + 1];
+    g[2 * i] = a;
+    expo += a;
+  }
+  double lh[2];
+  const lhaf_status s = lhaf_rpt(C.data(), g.data(), n, M, lh);
+  if (s != LHAF_OK) return s;
+  out[0] = std::exp(-expo) * lh[0] / fact;
+  out[1] = std::exp(-expo) * lh[1] / fact;
   return LHAF_OK;
 }
 

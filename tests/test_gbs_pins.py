@@ -88,3 +88,22 @@ def test_host_algebra_multimode(lib):
 def test_host_algebra_errors(lib):
     with pytest.raises(lib.LhafError):
         lib.lhaf_gbs_matrices(np.zeros((2, 2)) - 0.5 * np.eye(2), np.zeros(2))   # sigma_Q = 0
+
+
+def test_oracle_ips_single_mode(orc):
+    # one mode: n photons = singles ~ Poisson(|a|^2) plus 2 x pairs ~ Poisson(|b|^2 / 2)
+    a, b = 0.7 + 0.2j, 0.9 - 0.4j
+    la, lb = abs(a) ** 2, abs(b) ** 2 / 2
+    for n in range(0, 10):
+        want = sum(math.exp(-la) * la ** (n - 2 * m) / math.factorial(n - 2 * m)
+                   * math.exp(-lb) * lb ** m / math.factorial(m) for m in range(n // 2 + 1))
+        got = orc.ips_prob(np.array([[b]]), np.array([a]), [n])
+        assert abs(got - want) <= 1e-14 * max(1.0, want), (n, got, want)
+
+
+def test_oracle_ips_sum_rule(orc):
+    rng = G.rng_for(560)
+    B = G.random_symmetric(2, rng, 0.3)
+    al = G.complex_gaussian(2, 0.3, rng)
+    tot = sum(orc.ips_prob(B, al, [i, j]) for i in range(9) for j in range(9) if i + j <= 8)
+    assert 1.0 - 2e-5 < tot <= 1.0 + 1e-12, tot   # tail beyond |n| = 8: 8.5e-6

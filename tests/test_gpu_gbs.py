@@ -66,3 +66,18 @@ def test_gbs_sum_rule(lib):
             for c in range(7 - a - b):
                 tot += lib.lhaf_gbs_prob(sig, al, [a, b, c]).real
 
+
+
+def test_ips_prob_vs_oracle(lib, orc):
+    rng = G.rng_for(1560)
+    U = G.haar_unitary(4, rng)
+    B = G.pure_B(U, 0.6)
+    al = G.complex_gaussian(4, 0.4, rng)
+    for n in ([0, 0, 0, 0], [1, 0, 0, 0], [2, 1, 0, 1], [1, 1, 1, 1], [3, 0, 2, 0], [0, 4, 0, 1]):
+        want = orc.ips_prob(B, al, n)
+        assert rel(lib.lhaf_ips_prob(B, al, n), want) <= 1e-10, n
+    # sum rule through the product on 2 modes
+    B2 = G.random_symmetric(2, rng, 0.3)
+    a2 = G.complex_gaussian(2, 0.3, rng)
+    tot = sum(lib.lhaf_ips_prob(B2, a2, [i, j]) for i in range(11) for j in range(11) if i + j <= 10)
+    assert 1.0 - 1e-5 < tot <= 1.0 + 1e-12, tot   # tail beyond |n| = 10: 2.8e-6
