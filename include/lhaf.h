@@ -113,10 +113,17 @@ lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t
  * from 0 to the cutoff n_cut").  out[2 j], out[2 j + 1] = lhaf(A_n) for the pattern
  * reps_fixed with reps[mode] replaced by j, j = 0 .. n_cut.  A: k*k c128, gamma: k c128,
  * reps_fixed: k int32 (its entry at `mode` is ignored), 0 <= mode < k, 0 <= n_cut <= 64,
- * out: 2 (n_cut + 1) doubles.  All n_cut + 1 patterns are evaluated in ONE device job (one
- * sieve launch over their work units); the paper's further saving — one cubic step shared by
- * all counts of the batched mode — is not implemented yet (the per-count sieves are
- * independent).  Errors as lhaf_rpt_batch, plus LHAF_E_ARG for a bad mode / n_cut. */
+ * out: 2 (n_cut + 1) doubles.  The paper's shared evaluation: the fixed modes are matched once
+ * and the batched mode becomes a self-pair (mode, mode) with eta_b = floor((n_cut - p) / 2) in
+ * two groups by the parity p of its count (odd counts add one single-photon pair: with the
+ * fixed part's leftover photon, or with the phantom); every term (fixed-pair term, w_b in
+ * [-eta_b, eta_b]) is ONE Hessenberg reduction + La Budde + series to degree n_f + eta_b whose
+ * coefficients serve every count 2m + p with m >= |w_b|, m = w_b (mod 2), weighted by
+ * (-1)^k C(m, k), k = (m - w_b) / 2 (sieve_cut_v3).  One sieve launch, one finalize.
+ * n_cut = 64, or LHAF_CUTOFF_SEPARATE set in the environment, evaluates the n_cut + 1 patterns
+ * as independent sieves in one batch job instead (same values up to rounding: both orders
+ * carry the sieve's cancellation, ~kappa * eps per count).  Errors as lhaf_rpt_batch, plus
+ * LHAF_E_ARG for a bad mode / n_cut. */
 lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
                             int32_t k, int32_t mode, int32_t n_cut, double *out);
 

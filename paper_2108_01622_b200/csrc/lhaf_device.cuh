@@ -123,8 +123,13 @@ __device__ __forceinline__ int decode_term(const PatDesc &P, const JobDev &J, ui
     const int e = J.ipool[P.eta_off + lane];
     const uint64_t R = J.upool[P.radix_off + lane];
     kd = (int)((t / R) % (uint64_t)(e + 1));
-    w_s[lane] = e - 2 * kd;
-    fac = J.dpool[P.bin_off + J.ipool[P.eta_off + H + lane] + kd];
+    if ((P.flags & FLAG_CUT) && lane == H - 1) {
+      w_s[lane] = kd - P.eta_b;  // batched self-pair: w in [-eta_b, eta_b], sign and binomial
+      kd = 0;                    // belong to each count (applied by the caller)
+    } else {
+      w_s[lane] = e - 2 * kd;
+      fac = J.dpool[P.bin_off + J.ipool[P.eta_off + H + lane] + kd];
+    }
   }
   const unsigned odd = __ballot_sync(LHAF_FULL, (lane < H) && (kd & 1));
 #pragma unroll

@@ -110,6 +110,7 @@ struct Plan {
   int N = 0, H = 0, d = 0, n = 0, leftover = -1;
   uint64_t T = 1, T_eval = 0;
   std::vector<int> p, q, eta;  // q = -1 for the phantom
+  int eta_b = -1;              // >= 0: cutoff group (FLAG_CUT), the last pair is batched
 };
 
 lhaf_status make_plan(const int32_t *reps, int k, int mixed, Plan &P) {
@@ -222,6 +223,7 @@ struct lhaf_job {
   int e_max = 0, ntl_max = 0;   // v2: bordered dimension and leading coefficients
   bool any_loop = false;
   uint64_t units = 0, terms = 0, plan_bytes = 0;
+  uint64_t parts = 0;  // partial records (= units, except cutoff groups: (eta_b + 1) per unit)
   std::vector<PatDesc> descs;
   // device
   PatDesc *d_descs = nullptr;
@@ -264,8 +266,8 @@ static cudaError_t upload(T **dst, const std::vector<T> &v) {
 
 static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t gamma_stride,
                                    const int32_t *reps, int k, int batch, int mixed, bool on_device,
-                                   lhaf_job **out) {
-  if (!A || !gamma || !reps || !out) return fail(LHAF_E_ARG, "null pointer argument");
+                                   lhaf_job **out, const std::vector<Plan> *plans_in = nullptr) {
+  if (!A || !gamma || (!reps && !plans_in) || !out) return fail(LHAF_E_ARG, "null pointer argument");
   if (k < 0 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "k = %d out of range", k);
   if (batch < 0) return fail(LHAF_E_ARG, "batch = %d < 0", batch);
   const int kdim = mixed ? 2 * k : k;
@@ -297,11 +299,16 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   std::vector<double> dpool;
   std::vector<uint64_t> upool;
   int64_t cpool_words = 0;
-  uint64_t unit = 0;
+  uint64_t unit = 0, part = 0;
   j->descs.resize(batch);
   for (int b = 0; b < batch; ++b) {
     Plan P;
-    s = make_plan(reps + (size_t)b * k, k, mixed, P);
+    if (plans_in) {
+      P = (*plans_in)[b];
+      s = LHAF_OK;
+    } else {
+      s = make_plan(reps + (size_t)b * k, k, mixed, P);
+    }
     if (s == LHAF_OK) s = check_plan_limits(P);
     if (s != LHAF_OK) { job_free(j); return s; }
     PatDesc &D = j->descs[b];
@@ -326,10 +333,19 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     D.T_eval = P.T_eval;
     D.gamma_off = gamma_stride ? (int64_t)b * gamma_stride : 0;
     D.unit_begin = unit;
-    if (P.H == 0) { D.chunk = 0; D.units = 0; continue; }
-    D.chunk = chunk_for(P.T_eval);
+    D.part_base = (int64_t)part;
+    if (P.H == 0 || P.T_eval == 0) { D.chunk = 0; D.units = 0; continue; }
+    if (P.eta_b >= 0) {  // cutoff group: eta_b + 1 partials per unit, at most 4096 units
+      D.flags |= FLAG_CUT;
+      D.eta_b = P.eta_b;
+      D.chunk = std::max<uint64_t>(64, (P.T_eval + 4095) / 4096);
+      if (D.chunk > P.T_eval) D.chunk = P.T_eval;
+    } else {
+      D.chunk = chunk_for(P.T_eval);
+    }
     D.units = (P.T_eval + D.chunk - 1) / D.chunk;
     unit += D.units;
+    part += D.units * (uint64_t)(P.eta_b >= 0 ? P.eta_b + 1 : 1);
     j->terms += P.T_eval;
     j->d_max = std::max(j->d_max, P.d);
     j->n_max = std::max(j->n_max, P.n);
@@ -356,6 +372,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     cpool_words += (int64_t)(P.d + 1) * (P.d + 1) + 2 * P.d + 2;  // v1: Ct|uh|v|beta; v2: E x E
   }
   j->units = unit;
+  j->parts = part;
   j->plan_bytes = j->descs.size() * sizeof(PatDesc) + ipool.size() * 4 + dpool.size() * 8 +
                   upool.size() * 8;
   cudaError_t e = cudaSuccess;
@@ -364,8 +381,8 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   if (e == cudaSuccess) e = upload(&j->d_dpool, dpool);
   if (e == cudaSuccess) e = upload(&j->d_upool, upool);
   if (e == cudaSuccess) e = cudaMalloc(&j->d_cpool, std::max<int64_t>(1, cpool_words) * sizeof(double2));
-  if (e == cudaSuccess) e = cudaMalloc(&j->d_partials, std::max<uint64_t>(1, j->units) * sizeof(Partial));
-  if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->units) * sizeof(Partial));
+  if (e == cudaSuccess) e = cudaMalloc(&j->d_partials, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
+  if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
   if (e == cudaSuccess) e = cudaMalloc(&j->d_counter, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&j->d_out, std::max(1, batch) * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc(&j->d_abs, std::max(1, batch) * sizeof(double));
@@ -612,16 +629,90 @@ lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_s
 
 lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
                             int32_t k, int32_t mode, int32_t n_cut, double *out) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
   if (!A || !gamma || !reps_fixed || !out) return fail(LHAF_E_ARG, "null pointer argument");
   if (k < 1 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "k = %d out of range", k);
   if (mode < 0 || mode >= k) return fail(LHAF_E_ARG, "batched mode %d outside [0, %d)", mode, k);
   if (n_cut < 0 || n_cut > 64) return fail(LHAF_E_ARG, "n_cut = %d outside [0, 64]", n_cut);
-  std::vector<int32_t> reps((size_t)(n_cut + 1) * k);
-  for (int j = 0; j <= n_cut; ++j) {
-    memcpy(&reps[(size_t)j * k], reps_fixed, (size_t)k * sizeof(int32_t));
-    reps[(size_t)j * k + mode] = j;
+  std::vector<int32_t> rf(reps_fixed, reps_fixed + k);
+  rf[mode] = 0;
+  // App. B.5 shared evaluation: the fixed modes' matching plus the batched self-pair
+  // (mode, mode) with eta_b = floor((n_cut - parity) / 2), one group per parity of the count
+  Plan Pf;
+  lhaf_status s = make_plan(rf.data(), k, 0, Pf);
+  if (s != LHAF_OK) return s;
+  const bool shared = n_cut <= 63 && !getenv("LHAF_CUTOFF_SEPARATE") && g_ctx.variant == 0;
+  std::vector<Plan> groups;
+  int n_f[2] = {0, 0}, gidx[2] = {-1, -1};
+  if (shared) {
+    for (int par = 0; par < 2 && par <= n_cut; ++par) {
+      Plan G = Pf;
+      G.eta_b = (n_cut - par) / 2;
+      if (par == 1) {
+        if (Pf.leftover >= 0) {  // the leftover photon pairs with the batched one: no phantom
+          G.q.back() = mode;
+          G.leftover = -1;
+        }
+        else { G.p.push_back(mode); G.q.push_back(-1); G.eta.push_back(1); G.leftover = mode; }
+      }
+      int nf = 0;
+      uint64_t Tf = 1;
+      for (int e2 : G.eta) { nf += e2; Tf *= (uint64_t)(e2 + 1); }
+      G.p.push_back(mode); G.q.push_back(mode); G.eta.push_back(2 * G.eta_b);  // digit range
+      G.H = (int)G.eta.size();
+      G.d = 2 * G.H;
+      G.n = nf + G.eta_b;
+      G.N = Pf.N + par;
+      G.T = Tf * (uint64_t)(2 * G.eta_b + 1);
+      G.T_eval = G.T / 2;
+      n_f[par] = nf;
+      gidx[par] = (int)groups.size();
+      groups.push_back(G);
+    }
   }
-  return lhaf_rpt_batch(A, gamma, 0, reps.data(), k, n_cut + 1, out);
+  lhaf_job *j = nullptr;
+  if (shared) s = job_create_impl(A, gamma, 0, nullptr, k, (int)groups.size(), 0, false, &j, &groups);
+  if (!shared || (s == LHAF_OK && j->variant != 3)) {
+    if (j) { job_free(j); j = nullptr; }
+    std::vector<int32_t> reps((size_t)(n_cut + 1) * k);  // separate sieve per count
+    for (int c = 0; c <= n_cut; ++c) {
+      memcpy(&reps[(size_t)c * k], reps_fixed, (size_t)k * sizeof(int32_t));
+      reps[(size_t)c * k + mode] = c;
+    }
+    return lhaf_rpt_batch(A, gamma, 0, reps.data(), k, n_cut + 1, out);
+  }
+  if (s != LHAF_OK) return s;
+  // one sieve launch over both groups, then one finalize over n_cut + 1 virtual patterns
+  std::vector<PatDesc> vd(n_cut + 1);
+  for (int c = 0; c <= n_cut; ++c) {
+    const PatDesc &G = j->descs[gidx[c & 1]];
+    const int m = c >> 1;
+    PatDesc &D = vd[c];
+    memset(&D, 0, sizeof D);
+    D.d = (Pf.N + c == 0) ? 0 : 2;
+    D.n = n_f[c & 1] + m;
+    D.unit_begin = (uint64_t)G.part_base + (uint64_t)m * G.units;
+    D.units = G.units;
+  }
+  PatDesc *d_vd = nullptr;
+  double2 *d_o = nullptr;
+  cudaError_t e = upload(&d_vd, vd);
+  if (e == cudaSuccess) e = cudaMalloc(&d_o, (n_cut + 1) * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
+  if (e == cudaSuccess)
+    e = launch_sieve_cut_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, 0, j->units, g_ctx.num_sms, 0);
+  if (e == cudaSuccess) {
+    JobDev J = j->dev();
+    J.descs = d_vd;
+    J.npat = n_cut + 1;
+    e = launch_finalize(J, d_o, nullptr, 0);
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, d_o, (n_cut + 1) * sizeof(double2), cudaMemcpyDeviceToHost);
+  cudaFree(d_vd);
+  cudaFree(d_o);
+  job_free(j);
+  if (e != cudaSuccess) return fail(LHAF_E_CUDA, "cutoff job: %s", cudaGetErrorString(e));
+  return LHAF_OK;
 }
 
 lhaf_status lhaf_rpt(const double *A, const double *gamma, const int32_t *reps, int32_t k,

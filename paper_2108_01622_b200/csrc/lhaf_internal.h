@@ -22,9 +22,16 @@ struct PatDesc {
   int32_t radix_off;   // upool: R_h = prod_{h' < h} (eta_h' + 1)
   int64_t mat_off;     // cpool (double2): Ct[d*d] | uh[d] | v[d] | beta[1]
   int64_t gamma_off;   // offset (in complex entries) of this pattern's gamma row
+  // FLAG_CUT (cutoff group, App. B.5): the last pair is the batched self-pair; its digit
+  // j in [0, 2 eta_b] gives w = j - eta_b; outputs m = 0..eta_b (count 2m + parity) go to
+  // partials[part_base + m * units + unit - unit_begin]
+  int32_t eta_b;
+  int32_t pad_;
+  int64_t part_base;
 };
 
 constexpr uint32_t FLAG_LOOP = 1u;
+constexpr uint32_t FLAG_CUT = 2u;
 
 // Chunk partial: double-double complex sum of the unit's terms + sum |term|.
 struct Partial {
@@ -72,6 +79,9 @@ double v2_flops_per_term(int d, int n, bool loops);
 // Uses the v2 prep kernel (bordered column-swapped B0).
 cudaError_t launch_sieve_v3(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t unit_begin,
                             uint64_t unit_end, int num_sms, cudaStream_t s);
+// cutoff groups (FLAG_CUT patterns): one term serves every count of the batched mode
+cudaError_t launch_sieve_cut_v3(const JobDev &job, int e_max, int ntl_max, int n_max,
+                                uint64_t unit_begin, uint64_t unit_end, int num_sms, cudaStream_t s);
 cudaError_t launch_terms_v3(const JobDev &job, int e_max, int ntl_max, int n_max, const uint64_t *t,
                             int nt, double2 *g_out, cudaStream_t s);
 double v3_flops_per_term(int d, int n, bool loops);

@@ -841,6 +841,37 @@ __device__ __forceinline__ void team_reduce(const PatDesc &P, const Pattern &D, 
   LHAF_PHASE(1)
 }
 
+// a7: La Budde on the band T.hb into Q = T.u1 ([E+1][NTL], Q[j][t] = coefficient of
+// x^{deg q_j - t}); the whole team takes part (its first barrier orders the band writes).
+template <int NW, int TEAMS>
+__device__ __forceinline__ void team_labudde(const Pattern &D, const TeamMem &T, int tid, int team) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int n = D.n, E = D.E, NTL = D.NTL;
+  const double2 *hb = T.hb;
+  double2 *Q = T.u1;
+  double2 *part = Q + (E + 1) * NTL + 3 * (n + 2);  // [2][NW][2][NTL]
+  if constexpr (NW == 1) {
+    if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
+    else labudde<2>(hb, Q, E, NTL, lane);
+  } else {
+    // (two rows per barrier pays at NTL <= 32; one row per barrier above, measured)
+    if (NTL <= 32) labudde_team2<1, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
+    else labudde_team<2, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
+  }
+}
+
+// a8/a9 in one warp: series from c_B = q_0, c_M = q_1 (loops) or c_M = q_0; returns
+// g = [lam^n] and leaves Qs, Rs, Es (degrees 0..n) in the scratch after Q.
+__device__ __forceinline__ double2 warp_series(const Pattern &D, double2 *Q, int lane) {
+  const int n = D.n, E = D.E, NTL = D.NTL;
+  const double2 *cB = Q;
+  const double2 *cM = D.loops ? Q + NTL : Q;
+  double2 *scr = Q + (E + 1) * NTL;  // series scratch (3 (n+2))
+  if (n + 2 <= 32) return series<1>(cM, cB, n, NTL, D.loops, scr, lane);
+  if (n + 2 <= 64) return series<2>(cM, cB, n, NTL, D.loops, scr, lane);
+  return series<5>(cM, cB, n, NTL, D.loops, scr, lane);
+}
+
 // g(t) of one term (valid in warp 0 of the team); sign and weight from the decode (warp 0).
 template <int S, int CS, int NW, int TEAMS, bool CMP>
 __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J, uint64_t t,
@@ -850,32 +881,10 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
   long long t_last_ = clock64();
 #endif
   const int lane = tid & 31, warp = tid >> 5;
-  const int n = D.n, E = D.E, NTL = D.NTL;
-  const bool loops = D.loops;
-  const double2 *hb = T.hb;
-  double2 g = c0();
-  double2 *Q = T.u1;  // [E+1][NTL]: Q[j][t] = coefficient of x^{deg q_j - t}
-  {
-    double2 *part = Q + (E + 1) * NTL + 3 * (n + 2);  // [2][NW][NTL]
-    if constexpr (NW == 1) {
-      if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
-      else labudde<2>(hb, Q, E, NTL, lane);
-    } else {
-      // (two rows per barrier pays at NTL <= 32; one row per barrier above, measured)
-      if (NTL <= 32) labudde_team2<1, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
-      else labudde_team<2, NW, TEAMS>(hb, Q, part, E, NTL, warp, lane, team);
-    }
-  }
+  team_labudde<NW, TEAMS>(D, T, tid, team);
   LHAF_PHASE(3)
-  if (warp == 0) {
-    // ---- a8/a9: series from c_B = q_0, c_M = q_1 (loops) or c_M = q_0
-    const double2 *cB = Q;
-    const double2 *cM = loops ? Q + NTL : Q;
-    double2 *scr = Q + (E + 1) * NTL;  // series scratch (3 (n+2))
-    if (n + 2 <= 32) g = series<1>(cM, cB, n, NTL, loops, scr, lane);
-    else if (n + 2 <= 64) g = series<2>(cM, cB, n, NTL, loops, scr, lane);
-    else g = series<5>(cM, cB, n, NTL, loops, scr, lane);
-  }
+  double2 g = c0();
+  if (warp == 0) g = warp_series(D, T.u1, lane);
   LHAF_PHASE(4)
   team_sync<NW, TEAMS>(team);  // smem reused by the next term
   LHAF_PHASE(5)
@@ -932,6 +941,89 @@ sieve_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
       q.re_hi = a0; q.re_lo = a1; q.im_hi = a2; q.im_lo = a3; q.abs_hi = a4; q.abs_lo = a5;
       q.pad0 = 0; q.pad1 = 0;
       J.partials[u] = q;
+    }
+  }
+}
+
+// Cutoff groups (App. B.5; FLAG_CUT patterns built by lhaf_rpt_cutoff): the
+// last pair is the batched mode's self-pair with weight w_b = j - eta_b.  One reduction and
+// one series to degree n = n_f + eta_b per (fixed-pair term, w_b) serve every count 2m
+// (+ the group's parity) with m >= |w_b|, m = w_b (mod 2): lane m of warp 0 adds
+// (-1)^{k_b} C(m, k_b) [lam^{n_f + m}] f, k_b = (m - w_b) / 2, to its own accumulator; the
+// unit's partial of count m goes to partials[part_base + m * units + unit - unit_begin].
+template <int S, int CS, int NW, int TEAMS, int REGS, bool CMP>
+__global__ void __maxnreg__(REGS)
+sieve_cut_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
+  extern __shared__ double2 smem[];
+  __shared__ unsigned long long s_unit;
+  __shared__ double s_acc[TEAMS][32][6];
+  constexpr int TS = 32 * NW;
+  const int team = threadIdx.x / TS, tid = threadIdx.x % TS;
+  const int lane = tid & 31, warp = tid >> 5;
+  double2 *tbase = smem + (size_t)team * team_words;
+  for (int i = tid; i < team_words; i += TS) tbase[i] = c0();
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_unit = ubeg + atomicAdd(J.counter, 1ull);
+    __syncthreads();
+    const uint64_t u = s_unit;
+    if (u >= uend) break;
+    const PatDesc P = J.descs[find_pattern(J, u)];
+    const Pattern D = pattern_of(P);
+    const TeamMem T = carve<S, CS, NW>(tbase, D.E, D.NTL, D.n);
+    const uint64_t tb = (u - P.unit_begin) * P.chunk;
+    const uint64_t te = min(tb + P.chunk, P.T_eval);
+    const int eb = P.eta_b, nf = D.n - eb;
+    double rh = 0, rl = 0, ih = 0, il = 0, ah = 0, al = 0;
+    for (uint64_t t = tb + team; t < te; t += TEAMS) {
+      int sign = 1;
+      double weight = 1.0;
+      team_reduce<S, CS, NW, TEAMS, CMP>(P, D, J, t, T, tid, team, sign, weight);
+      team_labudde<NW, TEAMS>(D, T, tid, team);
+      if (warp == 0) {
+        warp_series(D, T.u1, lane);
+        __syncwarp();
+        const double2 *Qs = T.u1 + (D.E + 1) * D.NTL, *Es = Qs + 2 * (D.n + 2);
+        // the batched pair's weight, re-derived from t (T.wv is the reduction's position table)
+        const uint64_t Rb = J.upool[P.radix_off + D.H - 1];
+        const int wb = (int)((t / Rb) % (uint64_t)(2 * eb + 1)) - eb, m = lane;
+        if (m <= eb && m >= abs(wb) && ((m - wb) & 1) == 0) {
+          const int deg = nf + m;
+          double2 g;
+          if (D.loops) {
+            g = c0();
+            for (int i = 0; i <= deg; ++i) g = cfma(Qs[i], Es[deg - i], g);
+          } else {
+            g = Qs[deg];
+          }
+          const int kb = (m - wb) / 2;
+          double cb = 1.0;  // C(m, kb), exact
+          for (int i = 0; i < kb; ++i) cb = cb * (double)(m - i) / (double)(i + 1);
+          const double sw = (double)sign * weight * ((kb & 1) ? -cb : cb);
+          dd_add(rh, rl, sw * g.x);
+          dd_add(ih, il, sw * g.y);
+          dd_add(ah, al, weight * cb * hypot(g.x, g.y));
+        }
+      }
+      team_sync<NW, TEAMS>(team);  // smem reused by the next term
+    }
+    if (warp == 0) {
+      s_acc[team][lane][0] = rh; s_acc[team][lane][1] = rl; s_acc[team][lane][2] = ih;
+      s_acc[team][lane][3] = il; s_acc[team][lane][4] = ah; s_acc[team][lane][5] = al;
+    }
+    __syncthreads();
+    if (threadIdx.x <= eb) {
+      const int m = threadIdx.x;
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+      for (int w = 0; w < TEAMS; ++w) {
+        dd_add_dd(a0, a1, s_acc[w][m][0], s_acc[w][m][1]);
+        dd_add_dd(a2, a3, s_acc[w][m][2], s_acc[w][m][3]);
+        dd_add_dd(a4, a5, s_acc[w][m][4], s_acc[w][m][5]);
+      }
+      Partial q;
+      q.re_hi = a0; q.re_lo = a1; q.im_hi = a2; q.im_lo = a3; q.abs_hi = a4; q.abs_lo = a5;
+      q.pad0 = 0; q.pad1 = 0;
+      J.partials[P.part_base + (uint64_t)m * P.units + (u - P.unit_begin)] = q;
     }
   }
 }
@@ -1121,6 +1213,27 @@ struct Inst {
     kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw);
     return cudaGetLastError();
   }
+  static cudaError_t sieve_cut(const JobDev &job, int E, int NTL, int n, uint64_t ubeg,
+                               uint64_t uend, int num_sms, cudaStream_t s) {
+    const int tw = Sh::words(E, NTL, n);
+    const size_t smem = (size_t)tw * TEAMS * sizeof(double2);
+    auto *kern = sieve_cut_v3<S, CS, NW, TEAMS, REGS, CMP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t units = uend - ubeg;
+    uint64_t grid = (uint64_t)num_sms * per_sm;
+    if (grid > units) grid = units;
+    e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw);
+    return cudaGetLastError();
+  }
   static cudaError_t terms(const JobDev &job, int E, int NTL, int n, const uint64_t *t, int nt,
                            double2 *g_out, cudaStream_t s) {
     const int tw = Sh::words(E, NTL, n);
@@ -1266,6 +1379,19 @@ cudaError_t launch_sieve_v3(const JobDev &job, int e_max, int ntl_max, int n_max
   if (v3::alt_mode() == 11 && E > 48 && E <= v3::Y62::EMAX)
     return v3::Y62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
   LHAF_V3_DISPATCH(sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s))
+}
+
+cudaError_t launch_sieve_cut_v3(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t ubeg,
+                                uint64_t uend, int num_sms, cudaStream_t s) {
+  if (uend <= ubeg) return cudaSuccess;
+  cudaError_t e = v3::ensure_inv();
+  if (e != cudaSuccess) return e;
+  const int E = e_max;
+#define LHAF_CUT(I) \
+  if (E <= v3::I::EMAX) return v3::I::sieve_cut(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
+  LHAF_CUT(I9) LHAF_CUT(I17) LHAF_CUT(I25) LHAF_CUT(I32) LHAF_CUT(I48) LHAF_CUT(I62) LHAF_CUT(I64)
+#undef LHAF_CUT
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_terms_v3(const JobDev &job, int e_max, int ntl_max, int n_max, const uint64_t *t,

@@ -313,3 +313,34 @@ def test_cutoff_batched_chain_rule(lib, orc):
     assert rel(lib.lhaf_rpt_cutoff(A, g, fixed, 2, 0)[0], lib.lhaf_rpt(A, g, fixed)) <= 1e-15
     with pytest.raises(lib.LhafError):
         lib.lhaf_rpt_cutoff(A, g, fixed, k, 3)
+
+
+@pytest.mark.parametrize("fixed,mode,n_cut,loops", [
+    ([1, 2, 0, 1, 0, 1, 0, 0], 2, 9, True),     # odd N_f: the leftover photon pairs with mode 2
+    ([2, 0, 1, 1, 0, 0, 2, 0], 5, 12, True),    # even N_f: the odd counts get a phantom pair
+    ([1, 1, 0, 1, 0, 0, 0, 1], 0, 10, False),   # no loops: odd totals vanish
+    ([0] * 8, 3, 7, True),                      # nothing fixed: single-mode counts 0..7
+])
+def test_cutoff_shared_vs_oracle(lib, orc, fixed, mode, n_cut, loops):
+    # App. B.5 shared evaluation (one reduction per (fixed term, w_b) serving every count)
+    # against the oracle for each count, and against the per-count sieves
+    rng = G.rng_for(5230 + n_cut)
+    k = 8
+    A = G.pure_B(G.haar_unitary(k, rng), 0.75)
+    g = G.complex_gaussian(k, 0.35, rng) if loops else np.zeros(k, complex)
+    fixed = np.array(fixed, np.int32)
+    vals = lib.lhaf_rpt_cutoff(A, g, fixed, mode, n_cut)
+    os.environ["LHAF_CUTOFF_SEPARATE"] = "1"
+    try:
+        sep = lib.lhaf_rpt_cutoff(A, g, fixed, mode, n_cut)
+    finally:
+        del os.environ["LHAF_CUTOFF_SEPARATE"]
+    for c in range(n_cut + 1):
+        reps = fixed.copy()
+        reps[mode] = c
+        ref = orc.lhaf(A, g, reps)
+        if abs(ref) == 0.0:
+            assert abs(vals[c]) <= 1e-13 * max(1.0, max(abs(x) for x in sep)), (c, vals[c])
+            continue
+        assert rel(vals[c], ref) <= 1e-10, (c, vals[c], ref)
+        assert rel(vals[c], sep[c]) <= 1e-11, (c, vals[c], sep[c])
