@@ -127,6 +127,16 @@ lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t
 lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
                             int32_t k, int32_t mode, int32_t n_cut, double *out);
 
+/* The same loop hafnian by inclusion/exclusion over the pair copies instead of the +-1 sieve
+ * (the eigenvalue-trace formula ET_loop of P:403-415 with repeated pairs,
+ * the comparison of Fig. 5): lhaf = sum over c_h = 0..eta_h of
+ * (-1)^{n - sum c} prod C(eta_h, c_h) g(w = c), g as in the sieve.  Every term runs the same
+ * device path (Hessenberg + La Budde + series at full d; excluded pairs are zero columns, not
+ * deleted), there is no halving, so it evaluates prod (eta_h + 1) terms (twice the sieve's).
+ * Arguments, ownership and errors as lhaf_rpt. */
+lhaf_status lhaf_rpt_et(const double *A, const double *gamma, const int32_t *reps, int32_t k,
+                        double out[2]);
+
 /* Photon-number pattern probabilities of an M-mode Gaussian state (App. A,
  * P:301-320, Eq. (mixed_prob)):
  *   P(n | sigma, alpha) = exp(-alpha^dag sigma_Q^{-1} alpha / 2) / (sqrt(det sigma_Q) prod_i n_i!)

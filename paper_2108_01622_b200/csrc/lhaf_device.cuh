@@ -127,7 +127,7 @@ __device__ __forceinline__ int decode_term(const PatDesc &P, const JobDev &J, ui
       w_s[lane] = kd - P.eta_b;  // batched self-pair: w in [-eta_b, eta_b], sign and binomial
       kd = 0;                    // belong to each count (applied by the caller)
     } else {
-      w_s[lane] = e - 2 * kd;
+      w_s[lane] = (P.flags & FLAG_ET) ? e - kd : e - 2 * kd;
       fac = J.dpool[P.bin_off + J.ipool[P.eta_off + H + lane] + kd];
     }
   }

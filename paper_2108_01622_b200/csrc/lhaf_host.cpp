@@ -111,6 +111,7 @@ struct Plan {
   uint64_t T = 1, T_eval = 0;
   std::vector<int> p, q, eta;  // q = -1 for the phantom
   int eta_b = -1;              // >= 0: cutoff group (FLAG_CUT), the last pair is batched
+  bool et = false;             // inclusion/exclusion (FLAG_ET): T_eval = T
 };
 
 lhaf_status make_plan(const int32_t *reps, int k, int mixed, Plan &P) {
@@ -335,6 +336,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     D.unit_begin = unit;
     D.part_base = (int64_t)part;
     if (P.H == 0 || P.T_eval == 0) { D.chunk = 0; D.units = 0; continue; }
+    if (P.et) D.flags |= FLAG_ET;
     if (P.eta_b >= 0) {  // cutoff group: eta_b + 1 partials per unit, at most 4096 units
       D.flags |= FLAG_CUT;
       D.eta_b = P.eta_b;
@@ -713,6 +715,26 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
   job_free(j);
   if (e != cudaSuccess) return fail(LHAF_E_CUDA, "cutoff job: %s", cudaGetErrorString(e));
   return LHAF_OK;
+}
+
+lhaf_status lhaf_rpt_et(const double *A, const double *gamma, const int32_t *reps, int32_t k,
+                        double out[2]) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!A || !gamma || !reps || !out) return fail(LHAF_E_ARG, "null pointer argument");
+  if (k < 0 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "k = %d out of range", k);
+  std::vector<Plan> plans(1);
+  lhaf_status s = make_plan(reps, k, 0, plans[0]);
+  if (s != LHAF_OK) return s;
+  plans[0].et = true;
+  plans[0].T_eval = plans[0].H > 0 ? plans[0].T : 0;  // no halving: w -> -w is not a symmetry
+  lhaf_job *j = nullptr;
+  s = job_create_impl(A, gamma, 0, nullptr, k, 1, 0, false, &j, &plans);
+  if (s != LHAF_OK) return s;
+  double tmp[2];
+  s = evaluate(j, tmp, nullptr, 0);
+  job_free(j);
+  if (s == LHAF_OK) { out[0] = tmp[0]; out[1] = tmp[1]; }
+  return s;
 }
 
 lhaf_status lhaf_rpt(const double *A, const double *gamma, const int32_t *reps, int32_t k,

@@ -32,6 +32,9 @@ struct PatDesc {
 
 constexpr uint32_t FLAG_LOOP = 1u;
 constexpr uint32_t FLAG_CUT = 2u;
+// FLAG_ET: inclusion/exclusion over pair copies (ET) instead of the +-1 sieve:
+// w_h = eta_h - k_h, no halving, no 2^{-n} prefactor
+constexpr uint32_t FLAG_ET = 4u;
 
 // Chunk partial: double-double complex sum of the unit's terms + sum |term|.
 struct Partial {

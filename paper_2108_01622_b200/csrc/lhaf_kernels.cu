@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(128) finalize_kernel(JobDev J, double2 *out, d
     dd_add_dd(a2, a3, s[i][2], s[i][3]);
     dd_add_dd(a4, a5, s[i][4], s[i][5]);
   }
-  const int e = 1 - P.n;  // 2^{1-n}: halving (x2) and the 2^{-n} prefactor, exact
+  // 2^{1-n}: halving (x2) and the 2^{-n} prefactor, exact; 1 for inclusion/exclusion
+  const int e = (P.flags & FLAG_ET) ? 0 : 1 - P.n;
   out[p] = make_double2(ldexp(a0 + a1, e), ldexp(a2 + a3, e));
   if (abs_out) abs_out[p] = ldexp(a4 + a5, e);
 }

@@ -344,3 +344,24 @@ def test_cutoff_shared_vs_oracle(lib, orc, fixed, mode, n_cut, loops):
             continue
         assert rel(vals[c], ref) <= 1e-10, (c, vals[c], ref)
         assert rel(vals[c], sep[c]) <= 1e-11, (c, vals[c], sep[c])
+
+
+def test_et_inclusion_exclusion_vs_oracle(lib, orc):
+    # the same loop hafnian by inclusion/exclusion over pair copies
+    # (P:403-415), with repeats, odd N (phantom), no loops, and against the sieve at N = 32
+    rng = G.rng_for(403)
+    k = 7
+    A = G.random_symmetric(k, rng, 0.6)
+    g = G.complex_gaussian(k, 0.5, rng)
+    for reps in ([2, 1, 0, 3, 0, 1, 0], [1, 1, 1, 1, 1, 0, 0], [4, 0, 0, 0, 0, 0, 3], [0, 2, 2, 0, 1, 0, 2]):
+        ref = orc.lhaf(A, g, reps)
+        assert rel(lib.lhaf_rpt_et(A, g, reps), ref) <= 1e-10, reps
+    assert abs(lib.lhaf_rpt_et(A, np.zeros(k), [1, 1, 1, 0, 0, 0, 0])) <= 1e-14   # odd N, no loops
+    cfg = G.config(1)
+    assert rel(lib.lhaf_rpt_et(cfg["A"], cfg["gamma"], cfg["reps"]),
+               orc.lhaf(cfg["A"], cfg["gamma"], cfg["reps"], method="brute")) <= 1e-10
+    m = 32
+    A2 = G.random_symmetric(m, rng, 0.4)
+    g2 = G.complex_gaussian(m, 0.4, rng)
+    one = np.ones(m, np.int32)
+    assert rel(lib.lhaf_rpt_et(A2, g2, one), lib.lhaf_rpt(A2, g2, one)) <= 1e-9
