@@ -204,7 +204,9 @@ uint64_t chunk_for(uint64_t T_eval) {
     const uint64_t v = e ? strtoull(e, nullptr, 10) : 0;
     return v ? v : (uint64_t)131072;
   }();
-  const uint64_t min_chunk = 64;
+  // small sieves (< 2^16 terms: one latency-bound pattern) get 16-term units so that they
+  // spread over every SM; large ones keep >= 64 terms per unit to amortise the unit fetch
+  const uint64_t min_chunk = T_eval < 65536 ? 16 : 64;
   uint64_t c = (T_eval + max_units - 1) / max_units;
   if (c < min_chunk) c = min_chunk;
   if (c > T_eval) c = T_eval;
