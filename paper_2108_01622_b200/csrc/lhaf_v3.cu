@@ -1307,10 +1307,7 @@ using R62 = Inst<2, 31, 4, 1, 255, true>;
 // (LHAF_V3_ALT=6) single-phase reduction at 168 registers: 3 CTAs / SM for E <= 62
 using T62 = Inst<2, 31, 4, 1, 168>;
 // (LHAF_V3_ALT=8) v4: two reduction teams + one tail warp per CTA
-using V62 = Inst4<2, 31, 232, 40, false>;
-using W62 = Inst4<2, 31, 224, 56, false>;
-using X62 = Inst4<2, 31, 216, 72, false>;
-using Y62 = Inst4<2, 31, 208, 88, false>;
+using V62 = Inst4<2, 31, 208, 88, false>;  // (measured best of 232/40 .. 200/104)
 static int alt_mode() {
   static const int m = [] { const char *e = getenv("LHAF_V3_ALT"); return e ? atoi(e) : 0; }();
   return m;
@@ -1372,12 +1369,6 @@ cudaError_t launch_sieve_v3(const JobDev &job, int e_max, int ntl_max, int n_max
   const int E = e_max;
   if (v3::alt_mode() == 8 && E > 48 && E <= v3::V62::EMAX)
     return v3::V62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
-  if (v3::alt_mode() == 9 && E > 48 && E <= v3::W62::EMAX)
-    return v3::W62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
-  if (v3::alt_mode() == 10 && E > 48 && E <= v3::X62::EMAX)
-    return v3::X62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
-  if (v3::alt_mode() == 11 && E > 48 && E <= v3::Y62::EMAX)
-    return v3::Y62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
   LHAF_V3_DISPATCH(sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s))
 }
 
