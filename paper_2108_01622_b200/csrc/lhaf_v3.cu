@@ -41,6 +41,15 @@ static bool g_inv_ready = false;
 
 // Phase timing (diagnostic builds only, -DLHAF_PHASE_TIMING): cycles of thread 0 of every
 // team spent in decode/build, reduction, band -> F, La Budde, hand-off, end barrier.
+// Step probes (diagnostic builds only, -DLHAF_STEP_PROBE): clock64 of each warp leader of
+// block 0 at 7 points of every reduction step (the last term processed wins).
+#ifdef LHAF_STEP_PROBE
+__device__ long long g_probe[64][8][4];
+#define LHAF_SP(i) \
+  if (blockIdx.x == 0 && lane == 0 && warp < 4 && k < 64) g_probe[k][i][warp] = clock64();
+#else
+#define LHAF_SP(i)
+#endif
 #ifdef LHAF_PHASE_TIMING
 __device__ unsigned long long g_phase[8];
 #define LHAF_PHASE(i)                                             \
@@ -514,11 +523,12 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
   double2 *kbuf = cand + 2 * NW * CC;                             // [2][RC]
   unsigned *keys = reinterpret_cast<unsigned *>(kbuf + 2 * RC);   // [2][NW][4]
   for (int k = k0; k < k1; ++k) {
-    double2 *cb = cand + st.buf * NW * CC;
+    double2 *cb = cand + st.buf * NW * CC;  // (one row used: the pivot row)
     double2 *kb = kbuf + st.buf * RC;
     unsigned *yk = keys + st.buf * NW * 4;
     double2 *yv = reinterpret_cast<double2 *>(keys + 2 * NW * 4) + st.buf * NW * 2;
     st.buf ^= 1;
+    LHAF_SP(0)
     const bool candr = st.label > k && st.label < E;
     unsigned key = 0u;
     if (candr) {
@@ -526,11 +536,14 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
       key = (((fbits >> 6) + 1u) << 6) | (unsigned)(63 - st.label);
     }
     const unsigned wkey = __reduce_max_sync(LHAF_FULL, key);
+    LHAF_SP(1)
     if (par == 0 && st.mypos >= 0) kb[st.mypos] = candr ? st.colv : c0();
-    if (candr && key == wkey) {  // this warp's best row publishes itself (and 1 / its pivot)
-      double2 *dst = cb + warp * CC + par;
+    if (candr && key == wkey) {  // this warp's best row: its pivot record (and 1 / pivot)
+      if constexpr (NW == 1) {   // (one warp: it is the pivot row, publish at once)
+        double2 *dst = cb + par;
 #pragma unroll
-      for (int s = 0; s < CSP; ++s) dst[S * s] = A[s];
+        for (int s = 0; s < CSP; ++s) dst[S * s] = A[s];
+      }
       if (par == 0) {
         yv[2 * warp] = st.colv;
         if constexpr (NW > 1) yv[2 * warp + 1] = crecip(st.colv);
@@ -539,7 +552,9 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
       }
     }
     if (lane == 0) yk[4 * warp] = wkey;
+    LHAF_SP(2)
     team_sync<NW, TEAMS>(team);
+    LHAF_SP(3)
 
     unsigned bkey = 0u;
     int wb = 0;
@@ -551,6 +566,16 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
     const int plabel = 63 - (int)(bkey & 63u);
     const int p = (int)yk[4 * wb + 1];   // pivot: physical index
     const int qp = (int)yk[4 * wb + 2];  // and its column position
+    if constexpr (NW > 1) {
+      // only the team's pivot row publishes (one warp's stores instead of NW speculative rows
+      // contending for the shared-memory pipe), then a second barrier
+      if (rr == p && (bkey >> 6) > 1u) {
+        double2 *dst = cb + par;
+#pragma unroll
+        for (int s = 0; s < CSP; ++s) dst[S * s] = A[s];
+      }
+      team_sync<NW, TEAMS>(team);
+    }
     const int newlabel = (rr == p) ? k + 1 : (st.label == k + 1 ? plabel : st.label);
     if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL)
       hb[newlabel * NTL + k + 1 - newlabel] = (newlabel < st.zl) ? c0() : cmul(st.rs, st.colv);
@@ -558,7 +583,8 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
     if ((bkey >> 6) > 1u) {
       const double2 ip = (NW > 1) ? yv[2 * wb + 1] : crecip(yv[2 * wb]);
       const double2 m = (candr && rr != p) ? cmul(st.colv, ip) : c0();
-      const double2 *rp = cb + wb * CC + par;
+      LHAF_SP(4)
+      const double2 *rp = cb + par;  // the pivot row (position-indexed)
       const double2 *kq = kb + par;
       double xr0 = 0, xi0 = 0, yr0 = 0, yi0 = 0, xr1 = 0, xi1 = 0, yr1 = 0, yi1 = 0;
 #pragma unroll
@@ -576,10 +602,12 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
         }
       }
       double2 sum = make_double2((xr0 + xr1) - (xi0 + xi1), (yr0 + yr1) + (yi0 + yi1));
+      LHAF_SP(5)
 #pragma unroll
       for (int x = 1; x < S; x <<= 1) sum = cadd(sum, shfl2_xor(sum, x));
       st.colv = sum;  // column p scaled by the pivot: unit subdiagonal
       if (rr == p) st.rs = ip;
+      LHAF_SP(6)
     } else {
       st.colv = read_col<S, CSP>(A, qp, lane);  // nothing to eliminate: column p as it stands
       st.zl = k + 1;                            // H[k+1][k] = 0
@@ -1204,6 +1232,7 @@ struct Inst {
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
     if (e != cudaSuccess) return e;
+    if (const char *c = getenv("LHAF_CTAS_PER_SM")) per_sm = std::min(per_sm, atoi(c));  // diagnostics
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint64_t units = uend - ubeg;
     uint64_t grid = (uint64_t)num_sms * per_sm;
@@ -1327,6 +1356,12 @@ static cudaError_t ensure_inv() {
 
 cudaError_t v3_ensure_tables() { return v3::ensure_inv(); }
 
+#ifdef LHAF_STEP_PROBE
+extern "C" int lhaf_debug_step_probe(long long *out) {  // [64][8][4]
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out, v3::g_probe, sizeof(long long) * 64 * 8 * 4);
+}
+#endif
 #ifdef LHAF_PHASE_TIMING
 extern "C" int lhaf_debug_phase_cycles(unsigned long long *out8) {
   cudaDeviceSynchronize();
