@@ -42,6 +42,17 @@ lhaf_status fail(lhaf_status s, const char *fmt, ...) {
     if (e_ != cudaSuccess) return fail(LHAF_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
   } while (0)
 
+// Device memory for jobs comes from the device's default stream-ordered pool, configured in
+// ensure_device() to keep freed memory (no release threshold): creating and destroying a job
+// per call (lhaf_rpt*, the e2e path) then reuses pool memory instead of mapping new pages.
+template <class T>
+cudaError_t dmalloc(T **p, size_t bytes) {
+  return cudaMallocAsync((void **)p, bytes, 0);
+}
+inline void dfree(void *p) {
+  if (p) cudaFreeAsync(p, 0);
+}
+
 // ------------------------------------------------------------------ NCCL (dlopen)
 struct Nccl {
   void *h = nullptr;
@@ -100,6 +111,11 @@ lhaf_status ensure_device() {
                 prop.major, prop.minor);
   g_ctx.device = dev;
   g_ctx.num_sms = prop.multiProcessorCount;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~(uint64_t)0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   if (const char *e = getenv("LHAF_MAX_TERMS")) g_ctx.max_terms = strtoull(e, nullptr, 10);
   return LHAF_OK;
 }
@@ -194,7 +210,7 @@ lhaf_status check_symmetric(const double *A, int m) {
   return LHAF_OK;
 }
 
-uint64_t chunk_for(uint64_t T_eval) {
+uint64_t chunk_for(uint64_t T_eval, bool small_job) {
   // Terms per work unit: T_eval split into at most 2^17 units of >= 64 terms (independent
   // of the number of ranks, so results are bit-identical for any rank count; small enough
   // units that a 1/64 slice of a 2^29-term lhaf still spreads over every SM).  LHAF_MAX_UNITS
@@ -204,9 +220,9 @@ uint64_t chunk_for(uint64_t T_eval) {
     const uint64_t v = e ? strtoull(e, nullptr, 10) : 0;
     return v ? v : (uint64_t)131072;
   }();
-  // small sieves (< 2^16 terms: one latency-bound pattern) get 16-term units so that they
-  // spread over every SM; large ones keep >= 64 terms per unit to amortise the unit fetch
-  const uint64_t min_chunk = T_eval < 65536 ? 16 : 64;
+  // small jobs (< 2^16 terms in all: latency-bound) get 16-term units so that they spread
+  // over every SM; others keep >= 64 terms per unit to amortise the unit fetch and partials
+  const uint64_t min_chunk = small_job ? 16 : 64;
   uint64_t c = (T_eval + max_units - 1) / max_units;
   if (c < min_chunk) c = min_chunk;
   if (c > T_eval) c = T_eval;
@@ -251,17 +267,18 @@ struct lhaf_job {
 
 static void job_free(lhaf_job *j) {
   if (!j) return;
-  cudaFree(j->d_descs); cudaFree(j->d_ipool); cudaFree(j->d_dpool); cudaFree(j->d_upool);
-  cudaFree(j->d_cpool);
-  if (j->own_inputs) { cudaFree(j->d_A); cudaFree(j->d_gamma); }
-  cudaFree(j->d_partials); cudaFree(j->d_counter); cudaFree(j->d_out); cudaFree(j->d_abs);
+  cudaDeviceSynchronize();  // work on any stream may still use the buffers (as cudaFree did)
+  dfree(j->d_descs); dfree(j->d_ipool); dfree(j->d_dpool); dfree(j->d_upool);
+  dfree(j->d_cpool);
+  if (j->own_inputs) { dfree(j->d_A); dfree(j->d_gamma); }
+  dfree(j->d_partials); dfree(j->d_counter); dfree(j->d_out); dfree(j->d_abs);
   delete j;
 }
 
 template <class T>
 static cudaError_t upload(T **dst, const std::vector<T> &v) {
   const size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
-  cudaError_t e = cudaMalloc((void **)dst, bytes);
+  cudaError_t e = dmalloc(dst, bytes);
   if (e != cudaSuccess) return e;
   if (!v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
   return e;
@@ -303,6 +320,19 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   std::vector<uint64_t> upool;
   int64_t cpool_words = 0;
   uint64_t unit = 0, part = 0;
+  // the job's total term count decides the unit size (a function of the job only: results
+  // stay independent of the rank count)
+  bool small_job = true;
+  {
+    uint64_t tot = 0;
+    for (int b = 0; b < batch && small_job; ++b) {
+      Plan P;
+      if (plans_in) P = (*plans_in)[b];
+      else if (make_plan(reps + (size_t)b * k, k, mixed, P) != LHAF_OK) break;  // reported below
+      tot += P.T_eval;
+      if (tot >= 65536) small_job = false;
+    }
+  }
   j->descs.resize(batch);
   for (int b = 0; b < batch; ++b) {
     Plan P;
@@ -345,7 +375,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       D.chunk = std::max<uint64_t>(64, (P.T_eval + 4095) / 4096);
       if (D.chunk > P.T_eval) D.chunk = P.T_eval;
     } else {
-      D.chunk = chunk_for(P.T_eval);
+      D.chunk = chunk_for(P.T_eval, small_job);
     }
     D.units = (P.T_eval + D.chunk - 1) / D.chunk;
     unit += D.units;
@@ -384,19 +414,19 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   if (e == cudaSuccess) e = upload(&j->d_ipool, ipool);
   if (e == cudaSuccess) e = upload(&j->d_dpool, dpool);
   if (e == cudaSuccess) e = upload(&j->d_upool, upool);
-  if (e == cudaSuccess) e = cudaMalloc(&j->d_cpool, std::max<int64_t>(1, cpool_words) * sizeof(double2));
-  if (e == cudaSuccess) e = cudaMalloc(&j->d_partials, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
+  if (e == cudaSuccess) e = dmalloc(&j->d_cpool, std::max<int64_t>(1, cpool_words) * sizeof(double2));
+  if (e == cudaSuccess) e = dmalloc(&j->d_partials, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
   if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
-  if (e == cudaSuccess) e = cudaMalloc(&j->d_counter, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMalloc(&j->d_out, std::max(1, batch) * sizeof(double2));
-  if (e == cudaSuccess) e = cudaMalloc(&j->d_abs, std::max(1, batch) * sizeof(double));
+  if (e == cudaSuccess) e = dmalloc(&j->d_counter, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = dmalloc(&j->d_out, std::max(1, batch) * sizeof(double2));
+  if (e == cudaSuccess) e = dmalloc(&j->d_abs, std::max(1, batch) * sizeof(double));
   if (on_device) {
     j->own_inputs = false;
     j->d_A = (double2 *)A;
     j->d_gamma = (double2 *)gamma;
   } else {
-    if (e == cudaSuccess) e = cudaMalloc(&j->d_A, std::max<size_t>(1, (size_t)kdim * kdim) * sizeof(double2));
-    if (e == cudaSuccess) e = cudaMalloc(&j->d_gamma, std::max<size_t>(1, gamma_len) * sizeof(double2));
+    if (e == cudaSuccess) e = dmalloc(&j->d_A, std::max<size_t>(1, (size_t)kdim * kdim) * sizeof(double2));
+    if (e == cudaSuccess) e = dmalloc(&j->d_gamma, std::max<size_t>(1, gamma_len) * sizeof(double2));
     if (e == cudaSuccess && kdim > 0)
       e = cudaMemcpy(j->d_A, A, (size_t)kdim * kdim * sizeof(double2), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && gamma_len > 0)
@@ -596,8 +626,8 @@ lhaf_status lhaf_job_terms(lhaf_job *j, const uint64_t *t, int32_t nt, double *g
   if (j->batch < 1 || j->descs[0].d == 0) return fail(LHAF_E_ARG, "pattern 0 has no terms");
   uint64_t *dt = nullptr;
   double2 *dg = nullptr;
-  CUDA_TRY(cudaMalloc(&dt, std::max(1, nt) * sizeof(uint64_t)));
-  CUDA_TRY(cudaMalloc(&dg, std::max(1, nt) * sizeof(double2)));
+  CUDA_TRY(dmalloc(&dt, std::max(1, nt) * sizeof(uint64_t)));
+  CUDA_TRY(dmalloc(&dg, std::max(1, nt) * sizeof(double2)));
   cudaError_t e = cudaMemcpy(dt, t, nt * sizeof(uint64_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
     const PatDesc &D0 = j->descs[0];
@@ -606,8 +636,8 @@ lhaf_status lhaf_job_terms(lhaf_job *j, const uint64_t *t, int32_t nt, double *g
                             : launch_terms(j->dev(), j->variant, D0.d, D0.n, dt, nt, dg, 0);
   }
   if (e == cudaSuccess) e = cudaMemcpy(g_out, dg, nt * sizeof(double2), cudaMemcpyDeviceToHost);
-  cudaFree(dt);
-  cudaFree(dg);
+  dfree(dt);
+  dfree(dg);
   if (e != cudaSuccess) return fail(LHAF_E_CUDA, "lhaf_job_terms: %s", cudaGetErrorString(e));
   return LHAF_OK;
 }
@@ -701,7 +731,7 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
   PatDesc *d_vd = nullptr;
   double2 *d_o = nullptr;
   cudaError_t e = upload(&d_vd, vd);
-  if (e == cudaSuccess) e = cudaMalloc(&d_o, (n_cut + 1) * sizeof(double2));
+  if (e == cudaSuccess) e = dmalloc(&d_o, (n_cut + 1) * sizeof(double2));
   if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
   if (e == cudaSuccess)
     e = launch_sieve_cut_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, 0, j->units, g_ctx.num_sms, 0);
@@ -712,8 +742,8 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
     e = launch_finalize(J, d_o, nullptr, 0);
   }
   if (e == cudaSuccess) e = cudaMemcpy(out, d_o, (n_cut + 1) * sizeof(double2), cudaMemcpyDeviceToHost);
-  cudaFree(d_vd);
-  cudaFree(d_o);
+  dfree(d_vd);
+  dfree(d_o);
   job_free(j);
   if (e != cudaSuccess) return fail(LHAF_E_CUDA, "cutoff job: %s", cudaGetErrorString(e));
   return LHAF_OK;
