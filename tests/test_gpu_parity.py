@@ -365,3 +365,35 @@ def test_et_inclusion_exclusion_vs_oracle(lib, orc):
     g2 = G.complex_gaussian(m, 0.4, rng)
     one = np.ones(m, np.int32)
     assert rel(lib.lhaf_rpt_et(A2, g2, one), lib.lhaf_rpt(A2, g2, one)) <= 1e-9
+
+
+@pytest.mark.parametrize("c,last", [
+    (4, True), (4, False),
+    pytest.param(5, False, marks=pytest.mark.xfail(strict=True, reason=(
+        "cfg5 terms are ill-conditioned in FP64: the map from characteristic-polynomial "
+        "coefficients to g has condition ~5e8 (DESIGN.md 6, cfg5 conditioning)"))),
+])
+def test_full_size_sieve_unit_vs_oracle(lib, orc, c, last):
+    # The bench's own launch (the sieve kernel instance, work-unit layout and finalize) at the
+    # BASELINE config's full size, on one work unit: 2^{1-n} times the oracle's long-double
+    # sum of the same term range (halving C6).  Tolerance: per-term accuracy (1e-13
+    # relative) times sum |term| of the unit.  cfg5 is a strict xfail: its
+    # terms are ill-conditioned in FP64 (per-term errors 1e-6..1e-4 in every kernel variant,
+    # full-sum kappa ~ 2e9, "cfg5 conditioning").
+    cfg = G.config(c)
+    info = lib.lhaf_plan(cfg["reps"], mixed=cfg["mixed"])
+    job = lib.Job(cfg["A"], cfg["gamma"], cfg["reps"], mixed=cfg["mixed"])
+    U = job.units
+    chunk = max(64, -(-info.T_eval // 131072))
+    assert U == -(-info.T_eval // chunk)
+    u = U - 1 if last else 0
+    t0, t1 = u * chunk, min(info.T_eval, (u + 1) * chunk)
+    job.reset()
+    job.run(u, u + 1)
+    got = job.finalize()[0]
+    sabs = job.abs_sum()[0]
+    job.close()
+    s, cnt = orc.fds_range(cfg["A"], cfg["gamma"], cfg["reps"], t0, t1, mixed=cfg["mixed"])
+    assert cnt == t1 - t0
+    want = s * 2.0 ** (1 - info.n)
+    assert abs(got - want) <= 1e-12 * sabs, (c, u, got, want, sabs)
