@@ -59,7 +59,9 @@ typedef enum {
 
 /* Host-only plan of one pattern (S8(a) a2-a4).  Greedy matching of P:474-481 (reading C9:
  * stable sort by (count desc, mode asc) every round, n2 := 0 when one mode remains), the
- * phantom pair for odd N (reading C7), and the term counts.  mixed != 0 selects the natural
+ * phantom pair for odd N (reading C7), and the term counts.  mixed = 1 plans the mixed state
+ * by the same greedy matching of the doubled pattern (reps, reps) over the 2k modes (reading
+ * C11b: same value, measured far better conditioned in FP64); mixed = 2 selects the natural
  * pairing (i, i+k) x reps_i of P:425-428 (reading C11). */
 typedef struct {
   int32_t N;            /* photons = sum reps */
@@ -102,9 +104,10 @@ lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_s
                            const int32_t *reps, int32_t k, int32_t batch, double *out);
 
 /* Mixed-state loop hafnian (S8(a) a13): lhaf of the 2N x 2N A_n formed from the 2k x 2k
- * matrix A2 by repeating rows/cols i and i+k reps[i] times, evaluated with the
- * natural pairing (i, i+k) x reps_i.  A2: 2k*2k c128, gamma2: 2k c128,
- * reps: k int32. */
+ * matrix A2 by repeating rows/cols i and i+k reps[i] times.  Evaluated with the
+ * greedy matching of the doubled pattern (mixed mode 1, reading C11b); the natural pairing
+ * (i, i+k) x reps_i of P:425-428 is mixed mode 2 of the job API.  A2: 2k*2k c128,
+ * gamma2: 2k c128, reps: k int32. */
 lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t *reps,
                            int32_t k, double out[2]);
 
@@ -181,8 +184,9 @@ lhaf_status lhaf_rpt_batch_dev(const double *A_dev, const double *gamma_dev, int
                                double *out_dev, void *stream);
 
 /* ---- Jobs: a planned, device-resident evaluation (for timing and multi-rank control) ----
- * lhaf_job_create plans and uploads a batch (mixed != 0: natural pairing over A2 / gamma2,
- * each reps row of length k).  lhaf_job_run evaluates work units [unit_begin, unit_end) into
+ * lhaf_job_create plans and uploads a batch (mixed = 1: the mixed state over A2 / gamma2 by
+ * the greedy matching of the doubled pattern, mixed = 2: by the natural pairing; each reps
+ * row of length k).  lhaf_job_run evaluates work units [unit_begin, unit_end) into
  * the job's chunk-partial array (zeroed by lhaf_job_reset); lhaf_job_finalize sums the
  * partials in chunk order (double-double) and writes batch*2 doubles to out (host pointer if
  * out_is_device == 0).  One work unit = a fixed, rank-independent chunk of one pattern's

@@ -164,7 +164,7 @@ def version() -> str:
     return _lib.lhaf_version().decode()
 
 
-def lhaf_plan(reps, mixed: bool = False) -> PlanInfo:
+def lhaf_plan(reps, mixed: int = 0) -> PlanInfo:
     reps = _i32(reps)
     info = PlanInfo()
     _check(_lib.lhaf_plan(_ip(reps), reps.shape[0], int(mixed), ctypes.byref(info)))
@@ -266,7 +266,7 @@ class Job:
     """A planned, device-resident evaluation (lhaf_job_*).  Inputs are copied to HBM at
     creation; ``run`` evaluates a work-unit range into the chunk-partial array."""
 
-    def __init__(self, A, gamma, reps_batch, mixed: bool = False, gamma_per_pattern: bool = False):
+    def __init__(self, A, gamma, reps_batch, mixed: int = 0, gamma_per_pattern: bool = False):
         self._A, self._g, self._reps = _c128(A), _c128(gamma), _i32(reps_batch)
         if self._reps.ndim == 1:
             self._reps = self._reps[None, :]

@@ -140,7 +140,17 @@ lhaf_status make_plan(const int32_t *reps, int k, int mixed, Plan &P) {
   if (mixed) N *= 2;
   if (N > 4 * LHAF_MAX_DEGREE) return fail(LHAF_E_TOO_LARGE, "N = %ld photons too large", N);
   P.N = (int)N;
-  if (mixed) {
+  if (mixed == 1) {
+    // mixed state, default: the greedy matching of the doubled pattern (reps, reps) over the
+    // 2k modes (the same lhaf as the natural pairing; far better conditioned in FP64 -- the
+    // BASELINE cfg5 sum is rounding noise with the natural pairing)
+    std::vector<int32_t> r2(2 * (size_t)k);
+    for (int i = 0; i < k; ++i) r2[i] = r2[i + k] = reps[i];
+    lhaf_status s = make_plan(r2.data(), 2 * k, 0, P);
+    P.N = (int)N;
+    return s;
+  }
+  if (mixed) {  // mixed == 2: the natural pairing (i, i+k) x reps_i of P:425-428
     for (int i = 0; i < k; ++i)
       if (reps[i] > 0) { P.p.push_back(i); P.q.push_back(i + k); P.eta.push_back(reps[i]); }
   } else {

@@ -117,7 +117,9 @@ def test_per_term_parity(lib, orc):
     c2 = G.config(2)
     cases.append((dict(A=c2["A"], gamma=c2["gamma"], reps=c2["reps_batch"][0]), False))
     for cfg, mixed in cases:
-        C, v, eta, n = orc.reduced_system(cfg["A"], cfg["gamma"], cfg["reps"], mixed=mixed)
+        # mixed states are planned by the greedy matching of the doubled pattern (C11b)
+        reps_o = np.concatenate([cfg["reps"], cfg["reps"]]) if mixed else cfg["reps"]
+        C, v, eta, n = orc.reduced_system(cfg["A"], cfg["gamma"], reps_o, mixed=False)
         info = lib.lhaf_plan(cfg["reps"], mixed=mixed)
         assert info.etas() == eta and info.n == n
         job = lib.Job(cfg["A"], cfg["gamma"], cfg["reps"], mixed=mixed)
@@ -367,19 +369,14 @@ def test_et_inclusion_exclusion_vs_oracle(lib, orc):
     assert rel(lib.lhaf_rpt_et(A2, g2, one), lib.lhaf_rpt(A2, g2, one)) <= 1e-9
 
 
-@pytest.mark.parametrize("c,last", [
-    (4, True), (4, False),
-    pytest.param(5, False, marks=pytest.mark.xfail(strict=True, reason=(
-        "cfg5 terms are ill-conditioned in FP64: the map from characteristic-polynomial "
-        "coefficients to g has condition ~5e8 (DESIGN.md 6, cfg5 conditioning)"))),
-])
+@pytest.mark.parametrize("c,last", [(4, True), (4, False), (5, True), (5, False)])
 def test_full_size_sieve_unit_vs_oracle(lib, orc, c, last):
     # The bench's own launch (the sieve kernel instance, work-unit layout and finalize) at the
     # BASELINE config's full size, on one work unit: 2^{1-n} times the oracle's long-double
     # sum of the same term range (halving C6).  Tolerance: per-term accuracy (1e-13
-    # relative) times sum |term| of the unit.  cfg5 is a strict xfail: its
-    # terms are ill-conditioned in FP64 (per-term errors 1e-6..1e-4 in every kernel variant,
-    # full-sum kappa ~ 2e9, "cfg5 conditioning").
+    # relative) times sum |term| of the unit.  cfg5 (mixed) is planned by the
+    # greedy matching of the doubled pattern (C11b), so the oracle sums the doubled pattern;
+    # with the natural pairing its terms are ill-conditioned in FP64.
     cfg = G.config(c)
     info = lib.lhaf_plan(cfg["reps"], mixed=cfg["mixed"])
     job = lib.Job(cfg["A"], cfg["gamma"], cfg["reps"], mixed=cfg["mixed"])
@@ -393,7 +390,8 @@ def test_full_size_sieve_unit_vs_oracle(lib, orc, c, last):
     got = job.finalize()[0]
     sabs = job.abs_sum()[0]
     job.close()
-    s, cnt = orc.fds_range(cfg["A"], cfg["gamma"], cfg["reps"], t0, t1, mixed=cfg["mixed"])
+    reps_o = np.concatenate([cfg["reps"], cfg["reps"]]) if cfg["mixed"] else cfg["reps"]
+    s, cnt = orc.fds_range(cfg["A"], cfg["gamma"], reps_o, t0, t1, mixed=False)
     assert cnt == t1 - t0
     want = s * 2.0 ** (1 - info.n)
     assert abs(got - want) <= 1e-12 * sabs, (c, u, got, want, sabs)

@@ -82,12 +82,13 @@ def test_plan_matches_oracle_random(lib, orc):
 
 
 def test_plan_mixed_natural_pairing(lib):
-    info = lib.lhaf_plan([2, 0, 3, 1], mixed=True)
+    info = lib.lhaf_plan([2, 0, 3, 1], mixed=2)   # the paper's natural pairing (C11)
     assert info.pairs() == [(0, 4), (2, 6), (3, 7)] and info.etas() == [2, 3, 1]
     assert info.T == 3 * 4 * 2 and info.n == 6 and info.N == 12
-    # greedy matching on the doubled pattern gives the same term count (reading C11)
+    # the default mixed plan is the greedy matching of the doubled pattern (C11b)
     g = lib.lhaf_plan([2, 0, 3, 1, 2, 0, 3, 1])
-    assert g.T == info.T
+    m = lib.lhaf_plan([2, 0, 3, 1], mixed=1)
+    assert m.pairs() == g.pairs() and m.etas() == g.etas() and m.N == 12 and m.n == 6
 
 
 def test_decode_bit_exact(lib, orc):
