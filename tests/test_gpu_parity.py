@@ -395,3 +395,25 @@ def test_full_size_sieve_unit_vs_oracle(lib, orc, c, last):
     assert cnt == t1 - t0
     want = s * 2.0 ** (1 - info.n)
     assert abs(got - want) <= 1e-12 * sabs, (c, u, got, want, sabs)
+
+
+def test_cutoff_limits_single_mode_closed_form(lib):
+    # one photon-number-resolved mode alone: lhaf of c photons with pair weight a and loop g is
+    # sum_m C(c, 2m) (2m-1)!! a^m g^(c-2m) (all matchings of c copies: m pairs, c-2m loops).
+    # n_cut = 63 is the largest shared evaluation (eta_b = 31: one lane per count), n_cut = 64
+    # falls back to per-count sieves; both must give the closed form for the low counts.
+    k = 3
+    A = np.zeros((k, k), complex)
+    A[1, 1] = 0.45 - 0.2j
+    g = np.array([0.0, 0.3 + 0.1j, 0.0])
+    fixed = np.zeros(k, np.int32)
+
+    def closed(c):
+        a, gg = A[1, 1], g[1]
+        return sum(math.comb(c, 2 * m) * dfact(2 * m - 1) * a ** m * gg ** (c - 2 * m) for m in range(c // 2 + 1))
+
+    for n_cut in (63, 64):
+        vals = lib.lhaf_rpt_cutoff(A, g, fixed, 1, n_cut)
+        assert vals.shape == (n_cut + 1,)
+        for c in range(17):
+            assert rel(vals[c], closed(c)) <= 1e-9, (n_cut, c, vals[c], closed(c))
