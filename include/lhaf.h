@@ -130,6 +130,16 @@ lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t
 lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
                             int32_t k, int32_t mode, int32_t n_cut, double *out);
 
+/* The same pattern under many loop vectors (the threshold chain rule's
+ * sub-detector batching): out[2 g], out[2 g + 1] = lhaf of (A, gammas row g,
+ * reps), g < ngamma.  A: k*k c128, gammas: ngamma*k c128 row-major, reps: k int32, out:
+ * 2 ngamma doubles.  One device job (the patterns share A, the plan and one sieve launch);
+ * the paper's further saving -- one Hessenberg / characteristic polynomial per term shared by
+ * all loop vectors -- is not implemented (each loop vector borders its own matrix).  Errors
+ * as lhaf_rpt_batch. */
+lhaf_status lhaf_rpt_multigamma(const double *A, const double *gammas, int32_t ngamma,
+                                const int32_t *reps, int32_t k, double *out);
+
 /* The same loop hafnian by inclusion/exclusion over the pair copies instead of the +-1 sieve
  * (the eigenvalue-trace formula ET_loop of P:403-415 with repeated pairs,
  * the comparison of Fig. 5): lhaf = sum over c_h = 0..eta_h of

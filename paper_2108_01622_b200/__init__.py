@@ -74,6 +74,7 @@ def _load() -> ctypes.CDLL:
         "lhaf_gbs_prob": ([dp, dp, ctypes.c_int32, ip, ctypes.c_int32, dp]),
         "lhaf_ips_prob": ([dp, dp, ctypes.c_int32, ip, dp]),
         "lhaf_rpt_et": ([dp, dp, ip, ctypes.c_int32, dp]),
+        "lhaf_rpt_multigamma": ([dp, dp, ctypes.c_int32, ip, ctypes.c_int32, dp]),
         "lhaf_rpt_batch_dev": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
                                 ctypes.c_int32, vp, vp]),
         "lhaf_job_create": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
@@ -132,6 +133,7 @@ def reload_library():
 # every symbol include/lhaf.h declares (checked by tests/test_capi.py)
 EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed", "lhaf_rpt_cutoff",
             "lhaf_gbs_matrices", "lhaf_gbs_prob", "lhaf_ips_prob", "lhaf_rpt_et",
+            "lhaf_rpt_multigamma",
             "lhaf_rpt_batch_dev", "lhaf_job_create", "lhaf_job_info_get", "lhaf_job_reset",
             "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_finalize", "lhaf_job_abs_sum",
             "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
@@ -224,6 +226,14 @@ def lhaf_gbs_prob(sigma, alpha, n, pure: bool = False) -> complex:
     out = np.zeros(2)
     _check(_lib.lhaf_gbs_prob(_dp(sigma), _dp(alpha), n.shape[0], _ip(n), 1 if pure else 0, _dp(out)))
     return complex(out[0], out[1])
+
+
+def lhaf_rpt_multigamma(A, gammas, reps) -> np.ndarray:
+    """lhaf of one pattern under each row of gammas (one device job)."""
+    A, gammas, reps = _c128(A), _c128(np.atleast_2d(gammas)), _i32(reps)
+    out = np.zeros(2 * gammas.shape[0])
+    _check(_lib.lhaf_rpt_multigamma(_dp(A), _dp(gammas), gammas.shape[0], _ip(reps), reps.shape[0], _dp(out)))
+    return out[0::2] + 1j * out[1::2]
 
 
 def lhaf_rpt_et(A, gamma, reps) -> complex:

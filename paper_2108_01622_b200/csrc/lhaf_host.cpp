@@ -759,6 +759,17 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
   return LHAF_OK;
 }
 
+lhaf_status lhaf_rpt_multigamma(const double *A, const double *gammas, int32_t ngamma,
+                                const int32_t *reps, int32_t k, double *out) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!A || !gammas || !reps || !out) return fail(LHAF_E_ARG, "null pointer argument");
+  if (ngamma < 0 || k < 0 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "bad ngamma / k");
+  // one job: the same pattern once per loop vector (rows of gammas), one sieve launch
+  std::vector<int32_t> r((size_t)std::max(1, ngamma) * k);
+  for (int g = 0; g < ngamma; ++g) memcpy(&r[(size_t)g * k], reps, (size_t)k * sizeof(int32_t));
+  return lhaf_rpt_batch(A, gammas, k, r.data(), k, ngamma, out);
+}
+
 lhaf_status lhaf_rpt_et(const double *A, const double *gamma, const int32_t *reps, int32_t k,
                         double out[2]) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);

@@ -417,3 +417,16 @@ def test_cutoff_limits_single_mode_closed_form(lib):
         assert vals.shape == (n_cut + 1,)
         for c in range(17):
             assert rel(vals[c], closed(c)) <= 1e-9, (n_cut, c, vals[c], closed(c))
+
+
+def test_multigamma_vs_oracle(lib, orc):
+    # SURVEY 8(f) row 2 (API level): one pattern, several loop vectors incl. gamma = 0
+    rng = G.rng_for(388)
+    k = 6
+    A = G.random_symmetric(k, rng, 0.6)
+    gs = np.stack([G.complex_gaussian(k, 0.5, rng) for _ in range(4)] + [np.zeros(k, complex)])
+    reps = [2, 1, 0, 1, 3, 1]
+    vals = lib.lhaf_rpt_multigamma(A, gs, reps)
+    assert vals.shape == (5,)
+    for g, v in zip(gs, vals):
+        assert rel(v, orc.lhaf(A, g, reps)) <= 1e-10
