@@ -580,11 +580,16 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
     if (par == 0 && newlabel <= k + 1 && k + 1 - newlabel < NTL)
       hb[newlabel * NTL + k + 1 - newlabel] = (newlabel < st.zl) ? c0() : cmul(st.rs, st.colv);
     st.live &= ~(1ull << p);
-    if ((bkey >> 6) > 1u) {
+    // NW > 1: one code path for A (a zero pivot runs the pass with m = 0, which leaves A
+    // unchanged) -- two paths that update A differently made the compiler re-shuffle every
+    // slot register at the loop back-edge (~2 CS moves per column); measured +2 % at d = 60.
+    // One-warp teams keep the branch (there the single path measured 20 % slower).
+    const bool elim = (bkey >> 6) > 1u;
+    if (NW > 1 || elim) {
       const double2 ip = (NW > 1) ? yv[2 * wb + 1] : crecip(yv[2 * wb]);
-      const double2 m = (candr && rr != p) ? cmul(st.colv, ip) : c0();
+      const double2 m = (elim && candr && rr != p) ? cmul(st.colv, ip) : c0();
       LHAF_SP(4)
-      const double2 *rp = cb + par;  // the pivot row (position-indexed)
+      const double2 *rp = cb + par;  // the pivot row (position-indexed; stale but finite if !elim)
       const double2 *kq = kb + par;
       double xr0 = 0, xi0 = 0, yr0 = 0, yi0 = 0, xr1 = 0, xi1 = 0, yr1 = 0, yi1 = 0;
 #pragma unroll
@@ -605,13 +610,16 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
       LHAF_SP(5)
 #pragma unroll
       for (int x = 1; x < S; x <<= 1) sum = cadd(sum, shfl2_xor(sum, x));
-      st.colv = sum;  // column p scaled by the pivot: unit subdiagonal
-      if (rr == p) st.rs = ip;
-      LHAF_SP(6)
-    } else {
+      if (elim) {
+        st.colv = sum;  // column p scaled by the pivot: unit subdiagonal
+        if (rr == p) st.rs = ip;
+      }
+    }
+    if (!elim) {
       st.colv = read_col<S, CSP>(A, qp, lane);  // nothing to eliminate: column p as it stands
       st.zl = k + 1;                            // H[k+1][k] = 0
     }
+    LHAF_SP(6)
     st.label = newlabel;
   }
 }
