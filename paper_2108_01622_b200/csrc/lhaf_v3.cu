@@ -11,10 +11,11 @@
 //   a6  Hessenberg reduction of B by Gauss transforms with partial pivoting, index 0 fixed
 //       (so the first step maps y -> beta e1 and carries z^T -> z^T L^{-1}: the "bordered"
 //       loop trick).  Rows and columns never move: index i gets its final Hessenberg position
-//       as a label.  Per column k one team barrier:
-//         pivot = warp REDUX-max of a packed (|B[r][k]|_1, label) key, then across warps;
-//         each warp's best row is published to smem; every row then does, in ONE fused pass
-//         over its live slots,
+//       as a label.  Per column k two team barriers (one for a one-warp team):
+//         pivot = warp REDUX-max of a packed (|B[r][k]|_1, label) key; each warp's best row
+//         writes a small record (and 1 / its pivot) before the first barrier, then the
+//         team's pivot row alone stores its row to smem before the second; every row then
+//         does, in ONE fused pass over its live slots,
 //             left   A[r][c] -= m_r A[p][c]          (m_r = B[r][k] / piv, 0 if r is done)
 //             right  acc     += A[r][c] B[c][k]      (B[c][k] = 0 unless c is remaining)
 //         and the new pivot column p = acc (scaled by piv: unit subdiagonal) is carried in
