@@ -47,7 +47,8 @@ WORKLOADS = {
     "cfg4": dict(cfg=4, slices=64, desc="BASELINE config 4: single n=60 loop hafnian, m=100 Haar, tanh r=0.9, gamma sigma=0.1, 60 distinct modes, 2^29 evaluated terms at d=60"),
     "cfg2": dict(cfg=2, slices=1, desc="BASELINE config 2: batch of 4096 loop hafnians, N=24 distinct modes of m=50, 2^11 evaluated terms each at d=24"),
     "cfg3": dict(cfg=3, slices=1, desc="BASELINE config 3: n=40 collision-heavy loop hafnian, 16 modes of m=100, gamma=0"),
-    "cfg5": dict(cfg=5, slices=128, desc="BASELINE config 5: mixed-state lhaf, 36 photons over 24 modes, eta=0.3, 2k=200, natural pairing, d=48"),
+    "cfg5": dict(cfg=5, slices=128, desc="BASELINE config 5: mixed-state lhaf, 36 photons over 24 modes, eta=0.3, 2k=200, greedy matching of the doubled pattern (DESIGN C11b), d=48"),
+    "n40": dict(cfg=40, slices=1, desc="supplementary N=40 collision-free point (SURVEY 8(d)): cfg4 construction with 40 distinct modes, d=40, 2^19 evaluated terms; one step = one whole loop hafnian"),
 }
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
 

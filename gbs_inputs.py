@@ -131,6 +131,15 @@ def config(cfg: int) -> dict:
         reps = np.zeros(100, np.int32)
         reps[modes] = mult
         return dict(name="cfg5_mixed_N36", A=A2, gamma=gamma2, reps=reps, mixed=True)
+    if cfg == 40:
+        # supplementary N = 40 collision-free point: cfg4's construction with
+        # 40 distinct modes (d = 40, 2^19 evaluated terms)
+        U = haar_unitary(100, rng)
+        A = pure_B(U, 0.9)
+        gamma = complex_gaussian(100, 0.1, rng)
+        reps = np.zeros(100, np.int32)
+        reps[rng.choice(100, 40, replace=False)] = 1
+        return dict(name="n40_distinct", A=A, gamma=gamma, reps=reps, mixed=False)
     raise ValueError(cfg)
 
 
