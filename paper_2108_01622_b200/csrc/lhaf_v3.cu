@@ -146,13 +146,13 @@ struct Shape {
   static constexpr int EMAX = RC < CC ? RC : CC;
   __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 6 * NW; }
   __host__ __device__ static int u1_words(int E, int NTL, int n) {
-    const int lab = (E + 1) * NTL + 3 * (n + 2) + 4 * NW * NTL;
+    const int lab = 3 * (n + 2) + 4 * NW * NTL;  // series scratch + La Budde partials
     const int cmp = RC * S * ((3 * CS + 3) / 4);  // phased reduction buffer
     int w = red_words() > lab ? red_words() : lab;
     return w > cmp ? w : cmp;
   }
   __host__ __device__ static int words(int E, int NTL, int n) {
-    return E * NTL + u1_words(E, NTL, n) + 32 + 32;
+    return (E + 2) * NTL + u1_words(E, NTL, n) + 32 + 32;  // band (+2 rows: La Budde's q)
   }
 };
 
@@ -166,7 +166,7 @@ template <int S, int CS, int NW>
 __device__ __forceinline__ TeamMem carve(double2 *b, int E, int NTL, int n) {
   using Sh = Shape<S, CS, NW>;
   TeamMem T;
-  T.hb = b; b += E * NTL;
+  T.hb = b; b += (E + 2) * NTL;
   T.u1 = b; b += Sh::u1_words(E, NTL, n);
   T.wv = reinterpret_cast<int *>(b); b += 32;
   T.ww = reinterpret_cast<double *>(b);
@@ -885,8 +885,9 @@ __device__ __forceinline__ void team_labudde(const Pattern &D, const TeamMem &T,
   const int lane = tid & 31, warp = tid >> 5;
   const int n = D.n, E = D.E, NTL = D.NTL;
   const double2 *hb = T.hb;
-  double2 *Q = T.u1;
-  double2 *part = Q + (E + 1) * NTL + 3 * (n + 2);  // [2][NW][2][NTL]
+  // q_j is stored in band row j+1, which La Budde has consumed by then (rows E, E+1 extra)
+  double2 *Q = T.hb + NTL;
+  double2 *part = T.u1 + 3 * (n + 2);  // [2][NW][2][NTL]
   if constexpr (NW == 1) {
     if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
     else labudde<2>(hb, Q, E, NTL, lane);
@@ -899,11 +900,12 @@ __device__ __forceinline__ void team_labudde(const Pattern &D, const TeamMem &T,
 
 // a8/a9 in one warp: series from c_B = q_0, c_M = q_1 (loops) or c_M = q_0; returns
 // g = [lam^n] and leaves Qs, Rs, Es (degrees 0..n) in the scratch after Q.
-__device__ __forceinline__ double2 warp_series(const Pattern &D, double2 *Q, int lane) {
+__device__ __forceinline__ double2 warp_series(const Pattern &D, const double2 *Q, double2 *scr,
+                                               int lane) {
   const int n = D.n, E = D.E, NTL = D.NTL;
   const double2 *cB = Q;
   const double2 *cM = D.loops ? Q + NTL : Q;
-  double2 *scr = Q + (E + 1) * NTL;  // series scratch (3 (n+2))
+  (void)E;
   if (n + 2 <= 32) return series<1>(cM, cB, n, NTL, D.loops, scr, lane);
   if (n + 2 <= 64) return series<2>(cM, cB, n, NTL, D.loops, scr, lane);
   return series<5>(cM, cB, n, NTL, D.loops, scr, lane);
@@ -921,7 +923,7 @@ __device__ double2 team_term(const PatDesc &P, const Pattern &D, const JobDev &J
   team_labudde<NW, TEAMS>(D, T, tid, team);
   LHAF_PHASE(3)
   double2 g = c0();
-  if (warp == 0) g = warp_series(D, T.u1, lane);
+  if (warp == 0) g = warp_series(D, T.hb + D.NTL, T.u1, lane);
   LHAF_PHASE(4)
   team_sync<NW, TEAMS>(team);  // smem reused by the next term
   LHAF_PHASE(5)
@@ -1018,9 +1020,9 @@ sieve_cut_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
       team_reduce<S, CS, NW, TEAMS, CMP>(P, D, J, t, T, tid, team, sign, weight);
       team_labudde<NW, TEAMS>(D, T, tid, team);
       if (warp == 0) {
-        warp_series(D, T.u1, lane);
+        warp_series(D, T.hb + D.NTL, T.u1, lane);
         __syncwarp();
-        const double2 *Qs = T.u1 + (D.E + 1) * D.NTL, *Es = Qs + 2 * (D.n + 2);
+        const double2 *Qs = T.u1, *Es = Qs + 2 * (D.n + 2);
         // the batched pair's weight, re-derived from t (T.wv is the reduction's position table)
         const uint64_t Rb = J.upool[P.radix_off + D.H - 1];
         const int wb = (int)((t / Rb) % (uint64_t)(2 * eb + 1)) - eb, m = lane;
