@@ -145,9 +145,12 @@ struct Shape {
   static constexpr int TS = 32 * NW, RC = TS / S, CC = S * CS;
   static constexpr int EMAX = RC < CC ? RC : CC;
   __host__ __device__ static int red_words() { return 2 * NW * CC + 2 * RC + 6 * NW; }
+  // warps whose rows share the compaction buffer at a time: half the team where shared memory
+  // limits the occupancy (NW = 3: the d = 48 instance, 4 CTAs/SM instead of 3), else all
+  __host__ __device__ static constexpr int cmp_warps() { return NW == 3 ? 2 : NW; }
   __host__ __device__ static int u1_words(int E, int NTL, int n) {
     const int lab = 3 * (n + 2) + 4 * NW * NTL;  // series scratch + La Budde partials
-    const int cmp = RC * S * ((3 * CS + 3) / 4);  // phased reduction buffer
+    const int cmp = cmp_warps() * 32 * ((3 * CS + 3) / 4);  // compaction buffer
     int w = red_words() > lab ? red_words() : lab;
     return w > cmp ? w : cmp;
   }
@@ -625,15 +628,20 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
   }
 }
 
-// Compaction of every row's live columns from CSA to CSB slots (see above).  ipos[q] = index
-// of the column at position q (-1: none); npos = the new position of each old one.
+// Compaction of every row's live columns from CSA to CSB slots (see above), in place: the
+// narrower array is the prefix A[0 .. CSB) of the same registers, and the rows pass through
+// the shared-memory buffer either all at once or, where shared memory limits the occupancy,
+// in two halves of the team (Shape::cmp_warps).  ipos[q] = index of the column at position q (-1: none);
+// npos = the new position of each old one.
 template <int S, int CS, int CSA, int CSB, int NW, int TEAMS>
-__device__ __forceinline__ void compact(const double2 (&Ain)[CSA], double2 (&B)[CSB], PhaseSt &st,
-                                        int *ipos, int *npos, double2 *u1, int tid, int team) {
+__device__ __forceinline__ void compact(double2 (&A)[CSA], PhaseSt &st, int *ipos, int *npos,
+                                        double2 *u1, int tid, int team) {
   using Sh = Shape<S, CS, NW>;
   constexpr int TS = Sh::TS, RC = Sh::RC;
   constexpr int NB = S * CSB;
-  const int rr = tid / S, par = tid % S;
+  constexpr int HW = Sh::cmp_warps(), HROWS = HW * 32 / S;
+  constexpr int NHALF = (NW + HW - 1) / HW;  // 1 or 2 passes
+  const int rr = tid / S, par = tid % S, warp = tid >> 5;
   const uint64_t live = st.live;
   const int L = __popcll(live);
   for (int q = tid; q < 64; q += TS) {
@@ -641,16 +649,22 @@ __device__ __forceinline__ void compact(const double2 (&Ain)[CSA], double2 (&B)[
     npos[q] = (i >= 0 && ((live >> i) & 1ull)) ? __popcll(live & ((1ull << i) - 1ull)) : -1;
   }
   team_sync<NW, TEAMS>(team);  // npos visible; the last column's shared-memory reads are done
-  double2 *row = u1 + (size_t)rr * NB;
+  const int h = warp >= HW ? 1 : 0;
+  double2 *row = u1 + (size_t)(rr - h * HROWS) * NB;
 #pragma unroll
-  for (int s = 0; s < CSA; ++s) {
-    const int np = npos[S * s + par];
-    if (np >= 0) row[np] = Ain[s];
+  for (int half = 0; half < NHALF; ++half) {
+    if (h == half) {
+#pragma unroll
+      for (int s = 0; s < CSA; ++s) {
+        const int np = npos[S * s + par];
+        if (np >= 0) row[np] = A[s];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < CSB; ++s) A[s] = (S * s + par < L) ? row[S * s + par] : c0();
+    }
+    team_sync<NW, TEAMS>(team);
   }
-  __syncwarp();
-#pragma unroll
-  for (int s = 0; s < CSB; ++s) B[s] = (S * s + par < L) ? row[S * s + par] : c0();
-  team_sync<NW, TEAMS>(team);
   // new position table, row ownership, and zero pivot-column slots without an owner (the next
   // column's barrier orders these writes before their readers)
   for (int i = tid; i < 64; i += TS) {
@@ -690,14 +704,14 @@ __device__ __forceinline__ void reduce_phased(double2 (&A)[CS], int &label, doub
   const int k3 = max(k2, min(kend, max(0, E - 1 - S * CS3)));
   const int k4 = max(k3, min(kend, max(0, E - 1 - S * CS4)));
   phase_steps<S, CS, CS, NW, TEAMS>(A, st, 0, k2, E, NTL, hb, u1, tid, team);
-  double2 A2[CS2];
-  compact<S, CS, CS, CS2, NW, TEAMS>(A, A2, st, ipos, npos, u1, tid, team);
+  compact<S, CS, CS, CS2, NW, TEAMS>(A, st, ipos, npos, u1, tid, team);
+  double2 (&A2)[CS2] = *reinterpret_cast<double2 (*)[CS2]>(&A);  // prefix views of A
   phase_steps<S, CS, CS2, NW, TEAMS>(A2, st, k2, k3, E, NTL, hb, u1, tid, team);
-  double2 A3[CS3];
-  compact<S, CS, CS2, CS3, NW, TEAMS>(A2, A3, st, ipos, npos, u1, tid, team);
+  compact<S, CS, CS2, CS3, NW, TEAMS>(A2, st, ipos, npos, u1, tid, team);
+  double2 (&A3)[CS3] = *reinterpret_cast<double2 (*)[CS3]>(&A);
   phase_steps<S, CS, CS3, NW, TEAMS>(A3, st, k3, k4, E, NTL, hb, u1, tid, team);
-  double2 A4[CS4];
-  compact<S, CS, CS3, CS4, NW, TEAMS>(A3, A4, st, ipos, npos, u1, tid, team);
+  compact<S, CS, CS3, CS4, NW, TEAMS>(A3, st, ipos, npos, u1, tid, team);
+  double2 (&A4)[CS4] = *reinterpret_cast<double2 (*)[CS4]>(&A);
   phase_steps<S, CS, CS4, NW, TEAMS>(A4, st, k4, kend, E, NTL, hb, u1, tid, team);
   // the last two columns: the carried one (label kend) and the last live one
   const int lb = st.label;
