@@ -19,9 +19,11 @@ C-ABI call (lhaf_rpt with host buffers: H2D copies of A/gamma/plan, D2H of the r
 one whole loop hafnian.  The roofline kernel time is measured with CUDA events around the
 sieve launches on the same stream.
 
-Multi-GPU: launched with torchrun; one process per GPU; NCCL communicator of the library
-bootstrapped through torch.distributed; each step's slice is split across ranks (strong
-scaling of a single lhaf, one ncclAllReduce of chunk partials per step).
+Multi-GPU: `--gpus N` without WORLD_SIZE re-launches itself through torchrun (one process per
+GPU; fails loudly if fewer than N GPUs are visible); the library's NCCL communicator is
+bootstrapped through torch.distributed.  Per step: each rank evaluates its share of the step's
+slice, then one ncclAllReduce of that slice's unit partials (exact: disjoint supports).  The
+per-rank work per step is fixed (slices = 64 / N for cfg4: weak scaling).
 
 `--impl reference` times the CPU oracle (oracle/, long double, OpenMP) on a bounded sample of
 the same workload's terms (rank 0 only).
@@ -184,6 +186,79 @@ def cpu_baseline_sample(cfg, reps, seconds_target=22.0):
             "sample": f"{c} consecutive sieve terms of the workload's pattern 0 via oracle.fds_range, {dt:.1f} s"}
 
 
+def slice_bounds(U, s, slices, rank, world):
+    """Units of step s: the slice [sb, se) of U work units and this rank's share [ub, ue)."""
+    s %= slices
+    sb, se = U * s // slices, U * (s + 1) // slices
+    return sb, se, sb + (se - sb) * rank // world, sb + (se - sb) * (rank + 1) // world
+
+
+def hot_path_step(job, s, U, slices, rank, world, stream, out_ptr, between=None):
+    """One pass of the hot path over step s's slice: zero the slice's partials, evaluate this
+    rank's share (a4-a11), all-reduce the slice (a12; exact, each unit is owned by one rank),
+    finalize (a12).  `between(ub, ue)` brackets the evaluation (kernel timing)."""
+    sb, se, ub, ue = slice_bounds(U, s, slices, rank, world)
+    job.reset_range(sb, se, stream)
+    if between:
+        between(ub, ue, True)
+    job.run(ub, ue, stream)
+    if between:
+        between(ub, ue, False)
+    job.allreduce_range(sb, se, stream)
+    job.finalize_dev(out_ptr, stream)
+
+
+def survey_flops_per_term(d, n):
+    """SURVEY 8(d)'s algorithmic work per sieve term (App. A.7): Householder Hessenberg
+    (40/3) d^3 + La Budde (4/3) d^3 + loop terms 4 min(n, d) d^2 + Newton 8 n d + series 4 n^2
+    real FP64 flops -- the declared model the roofline fraction is quoted against."""
+    return (40.0 / 3.0) * d ** 3 + (4.0 / 3.0) * d ** 3 + 4.0 * min(n, d) * d * d + 8.0 * n * d + 4.0 * n * n
+
+
+def relaunch_with_torchrun(n):
+    """bench.py --gpus N without WORLD_SIZE: start N ranks (one per GPU) through torchrun."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} requested but only {have} CUDA device(s) are visible"}), flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")       # NCCL init lines (transport, NVLS) on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def time_whole_lhaf(L, cfg_id, reps_override=None, repeats=5):
+    """Seconds per loop hafnian of a whole (small) instance through the job API, CUDA events
+    around run + finalize on one stream, median of `repeats` after one warm-up."""
+    import torch
+    c = G.config(cfg_id)
+    reps = c["reps"] if reps_override is None else reps_override
+    job = L.Job(c["A"], c["gamma"], reps, mixed=c["mixed"])
+    st = torch.cuda.current_stream()
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    times = []
+    for r in range(repeats + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        job.reset(st.cuda_stream)
+        job.run(0, job.units, st.cuda_stream)
+        job.finalize_dev(out.data_ptr(), st.cuda_stream)
+        b.record(st)
+        torch.cuda.synchronize()
+        if r:
+            times.append(a.elapsed_time(b) * 1e-3)
+    terms = job.terms
+    job.close()
+    return {"s_per_lhaf": float(np.median(times)), "terms": int(terms), "d": int(job.info.d_max),
+            "n": int(job.info.n_max), "terms_per_s": terms / float(np.median(times)), "repeats": repeats}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -195,16 +270,21 @@ def main():
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-n40", action="store_true")
     ap.add_argument("--ref-terms", type=int, default=256)
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
-    slices = args.slices or w["slices"]
     if args.steps is None:
         args.steps = 5
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch_with_torchrun(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        sys.exit(2)
 
     if args.impl == "reference":
         run_reference(args, rank)
@@ -212,6 +292,8 @@ def main():
 
     import torch
     import torch.distributed as dist
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"rank {rank}: no CUDA device {local} (visible: {torch.cuda.device_count()})")
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -223,36 +305,41 @@ def main():
         uid = [L.lhaf_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         L.lhaf_init_rank(rank, world, uid[0], local)
+        print(f"rank {rank}/{world}: library NCCL communicator up on cuda:{local}", file=sys.stderr, flush=True)
     else:
         L.lhaf_set_device(local)
 
     w, cfg, reps = load_workload(args.workload)
     job = L.Job(cfg["A"], cfg["gamma"], reps, mixed=cfg["mixed"])
     U = job.units
+    # A step is one slice of the lhaf's work units.  Per-rank work per step is held fixed as N
+    # grows (slices = base / N, each split across the N ranks: weak scaling, >= 2048 units per
+    # rank per step for cfg4); single-slice workloads (whole batch / whole lhaf per step) split
+    # the same work across the ranks (strong scaling).
+    base = args.slices or w["slices"]
+    slices = max(1, base // world)
+    scaling = "weak" if base >= world and base > 1 else "strong"
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     out_dev = torch.zeros(2 * job.info.batch, dtype=torch.float64, device="cuda")
 
-    def slice_units(s):
-        s %= slices
-        b, e = U * s // slices, U * (s + 1) // slices
-        return b + (e - b) * rank // world, b + (e - b) * (rank + 1) // world
-
     kernel_ev = []
+    pending = []
+
+    def kernel_events(ub, ue, start):
+        if start:
+            pending.append(torch.cuda.Event(enable_timing=True))
+            pending[-1].record(stream)
+        else:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record(stream)
+            kernel_ev.append((pending.pop(), b, ue - ub))
 
     def step(s, record=False):
         flush.fill_(float(s))
-        ub, ue = slice_units(s)
-        if record:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-        job.run(ub, ue, sp)
-        if record:
-            b.record(stream)
-            kernel_ev.append((a, b, ue - ub))
-        job.allreduce(sp)
-        job.finalize_dev(out_dev.data_ptr(), sp)
+        hot_path_step(job, s, U, slices, rank, world, sp, out_dev.data_ptr(),
+                      kernel_events if record else None)
 
     # warm-up
     job.reset(sp)
@@ -280,33 +367,43 @@ def main():
     if world > 1:
         t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kernel_ms_max = float(t[0]), float(t[1])
+        ms = float(t[0])
         tt = torch.tensor([my_terms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt)
         total_terms = float(tt[0])
     else:
-        kernel_ms_max = kernel_ms
         total_terms = my_terms
     value = total_terms / (ms * 1e-3)
     result = out_dev.cpu().numpy()
     full_cover = args.steps >= slices
     s_per_lhaf = (job.terms / value) if job.info.batch == 1 else None
 
-    # roofline: algorithmic FP64 flops per launch / launch duration, vs measured DFMA peak
-    flops_term = job.info.flops_per_term_model
+    # roofline of the dominant kernel (the sieve): algorithmic FP64 flops per launch (SURVEY
+    # 8(d)'s F per term x the launch's terms) / the launch's CUDA-event time, against the
+    # measured DFMA peak; the kernel's own executed-useful model and ncu's executed-flop
+    # fraction (profiles/, one full capture) next to it
+    d, n = int(job.info.d_max), int(job.info.n_max)
+    flops_term = survey_flops_per_term(d, n)
+    own_term = job.info.flops_per_term_model
     peak, peak_src = fp64_peak()
+    spec_peak = 148 * 64 * 2 * 1.965e9 / 1e12
     achieved = my_terms * flops_term / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else None
+    own = my_terms * own_term / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
-                "peak_source": peak_src, "flops_per_term": flops_term,
+                "peak_source": peak_src, "peak_spec": spec_peak,
+                "frac_of_spec": (achieved / spec_peak) if achieved else None,
+                "flops_per_term": flops_term, "flops_model": "SURVEY 8(d) F(d, n)",
+                "flops_per_term_kernel_useful": own_term,
+                "fp64_pct_model_kernel_useful": (own / peak) if own else None,
                 "kernel_share_of_step": kernel_ms / ms if ms > 0 else None}
-    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(traffic_file):
-        try:
-            tj = json.load(open(traffic_file))
-            roofline["traffic"] = tj.get(args.workload)
-        except Exception:
-            pass
+    for fname, key in (("traffic.json", "traffic"), ("ncu_fp64.json", "fp64_pct_ncu")):
+        fpath = os.path.join(ROOT, "profiles", fname)
+        if os.path.exists(fpath):
+            try:
+                roofline[key] = json.load(open(fpath)).get(args.workload)
+            except Exception:
+                pass
 
     # e2e: the public C-ABI with host buffers, every step: job create (H2D of A, gamma, plan),
     # run over the step's slice, finalize (D2H of the result); the batch: lhaf_rpt_batch
@@ -326,10 +423,9 @@ def main():
                 e2e_terms += job.terms * (rank == 0)
             else:
                 jb = L.Job(A, gm, reps, mixed=cfg["mixed"])
-                ub, ue = slice_units(s)
-                jb.reset()
+                sb, se, ub, ue = slice_bounds(U, s, slices, rank, world)
                 jb.run(ub, ue)
-                jb.allreduce()
+                jb.allreduce_range(sb, se)
                 v = jb.finalize()
                 e2e_terms += (ue - ub) * terms_per_unit
                 jb.close()
@@ -348,6 +444,16 @@ def main():
                "call": "lhaf_rpt_batch" if reps.ndim == 2 else "lhaf_job_create/run/allreduce/finalize (pinned host buffers)",
                "result_first": [complex(np.atleast_1d(v)[0]).real, complex(np.atleast_1d(v)[0]).imag]}
 
+    # the n = 40 point of the BASELINE metric: seconds per whole loop hafnian, measured (one
+    # GPU's worth of work; rank 0): the collision-free N = 40 instance (2^19 terms at d = 40)
+    # and cfg3 (N = 40 with collisions)
+    n40 = None
+    if rank == 0 and world == 1 and not args.no_n40 and args.workload == "cfg4":
+        try:
+            n40 = {"n40_distinct": time_whole_lhaf(L, 40), "cfg3_collisions": time_whole_lhaf(L, 3)}
+        except Exception as ex:
+            n40 = {"error": str(ex)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -356,19 +462,25 @@ def main():
             cpu = {"error": str(ex)}
 
     if rank == 0:
+        kappa = None
+        if full_cover and job.info.batch == 1:
+            kappa = float(job.abs_sum()[0] / max(abs(complex(result[0], result[1])), 1e-300))
         line = {
             "metric": "sieve terms/s", "value": value, "unit": "terms/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.workload, "desc": w["desc"], "slices": slices,
-                       "units": U, "terms_per_lhaf": job.terms, "d": job.info.d_max,
-                       "n": job.info.n_max, "kernel_variant": job.info.kernel,
+                       "units": U, "terms_per_lhaf": job.terms, "d": d, "n": n,
+                       "kernel_variant": job.info.kernel,
                        "l2": "256 MiB buffer written before every step (inside the timed region)",
                        "parallelism": f"term-range shards x{world}"},
             "s_per_lhaf": s_per_lhaf if full_cover else None,
             "s_per_lhaf_extrapolated": None if full_cover else s_per_lhaf,
             "result": [float(result[0]), float(result[1])] if full_cover and job.info.batch == 1 else None,
+            "accuracy": {"kappa": kappa,
+                         "pin": "tests/test_gpu_fullsize.py::test_block_diagonal_N60 (P10, P:510; same kernel instance at d = 60)"},
+            "n40": n40,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 2 * len(kernel_ev),
             "clocks": clk.summary(),

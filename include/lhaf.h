@@ -187,8 +187,10 @@ lhaf_status lhaf_ips_prob(const double *B, const double *alpha, int32_t M, const
 
 /* Same three entry points with DEVICE pointers for A / gamma / out (reps stays on the host,
  * since planning is host integer work) and an explicit cudaStream_t (passed as void*; NULL =
- * the legacy default stream).  The call is asynchronous with respect to the host only in the
- * sense that results land in out_dev on `stream`; it synchronises the stream before return. */
+ * the legacy default stream).  Ordering: the call first synchronises the device, so inputs
+ * written on any stream (e.g. a torch side stream) are complete before they are read; A is
+ * copied back for the symmetry check when 2k <= 2048.  Results land in out_dev on `stream`,
+ * which is synchronised before return. */
 lhaf_status lhaf_rpt_batch_dev(const double *A_dev, const double *gamma_dev, int64_t gamma_stride,
                                const int32_t *reps, int32_t k, int32_t batch, int32_t mixed,
                                double *out_dev, void *stream);
@@ -219,8 +221,19 @@ lhaf_status lhaf_job_create(const double *A, const double *gamma, int64_t gamma_
 lhaf_status lhaf_job_info_get(const lhaf_job *job, lhaf_job_info *info);
 lhaf_status lhaf_job_reset(lhaf_job *job, void *stream);
 lhaf_status lhaf_job_run(lhaf_job *job, uint64_t unit_begin, uint64_t unit_end, void *stream);
-/* All-reduce (sum) of the partial array over the ranks of lhaf_init_rank (no-op if 1 rank). */
+/* All-reduce (sum) of the partial array over the ranks of lhaf_init_rank (ncclAllReduce on
+ * `stream`; no-op for a single rank without a communicator).  Exact: the ranks' unit ranges are
+ * disjoint and every other entry is zero (x + 0 = x), so the finalized value is bit-identical
+ * for any rank count (S8(e) a12). */
 lhaf_status lhaf_job_allreduce(lhaf_job *job, void *stream);
+/* The same on the unit range [unit_begin, unit_end) only, plus a stream-ordered zeroing of that
+ * range: a caller that evaluates a long sieve slice by slice (bench.py) zeroes the slice,
+ * runs its own shard of it, and all-reduces just the slice (each unit is owned by one rank,
+ * so the sum is exact and the other units are untouched).  Errors: E_ARG if the range is not
+ * inside [0, units), E_STATE / E_NCCL as lhaf_job_allreduce. */
+lhaf_status lhaf_job_reset_range(lhaf_job *job, uint64_t unit_begin, uint64_t unit_end, void *stream);
+lhaf_status lhaf_job_allreduce_range(lhaf_job *job, uint64_t unit_begin, uint64_t unit_end,
+                                     void *stream);
 lhaf_status lhaf_job_finalize(lhaf_job *job, double *out, int32_t out_is_device, void *stream);
 /* Optional diagnostic: per-pattern sum_t |term_t| * 2^{1-n} (the conditioning denominator:
  * kappa = abs_sum / |lhaf|).  Valid after lhaf_job_finalize.  out: batch doubles (host). */
@@ -236,9 +249,14 @@ lhaf_status lhaf_job_terms(lhaf_job *job, const uint64_t *t, int32_t nt, double 
 /* ---- Devices and ranks ---- */
 /* Select the CUDA device of this process (default 0, or LHAF_DEVICE env). */
 lhaf_status lhaf_set_device(int32_t device);
-/* Multi-rank (one process per GPU).  Rank 0 calls lhaf_get_unique_id and broadcasts the 128
- * bytes (e.g. through torch.distributed); every rank then calls lhaf_init_rank.  NCCL is
- * loaded at run time (dlopen of libnccl.so.2). */
+/* Multi-rank (one process per GPU; "each term in the sum can be computed
+ * independently", S8(e)).  Rank 0 calls lhaf_get_unique_id and broadcasts the 128 bytes (e.g.
+ * through torch.distributed); every rank then calls lhaf_init_rank.  NCCL is loaded at run
+ * time (dlopen of libnccl.so.2).  nranks = 1 with id128 = NULL: a single rank without NCCL;
+ * nranks = 1 with an id: a one-rank NCCL communicator (the all-reduce then runs through
+ * ncclAllReduce exactly as with N ranks -- used to exercise that path on one GPU).
+ * Errors: E_ARG (rank outside [0, nranks), null id for nranks > 1), E_NCCL (dlopen or
+ * communicator creation failed; the context falls back to a single rank). */
 lhaf_status lhaf_get_unique_id(void *id128);
 lhaf_status lhaf_init_rank(int32_t rank, int32_t nranks, const void *id128, int32_t device);
 lhaf_status lhaf_rank_info(int32_t *rank, int32_t *nranks);
@@ -248,7 +266,9 @@ lhaf_status lhaf_rank_info(int32_t *rank, int32_t *nranks);
 lhaf_status lhaf_shard_units(uint64_t units, int32_t rank, int32_t nranks, uint64_t *begin,
                              uint64_t *end);
 
-/* Kernel override for experiments: 0 = automatic, else a variant id. */
+/* Kernel override for experiments and cross-checks: 0 = automatic (v5 for E > 32, v3 below),
+ * 1 = the Householder baseline (lhaf_kernels.cu), 3 = v3 for every size, 5 = v5 where it
+ * applies.  Errors: E_ARG for any other id. */
 lhaf_status lhaf_set_kernel(int32_t variant);
 
 const char *lhaf_last_error(void);

@@ -15,6 +15,9 @@ Parity status per function:
   lhaf_et           pinned: agreement with lhaf_brute (N <= 12) + closed forms to N = 40
   matched_reps      pinned: the paper's worked example n = (2,1,0,3) -> 6 terms
   fds_term          pinned: 2x2 closed form; full-sum agreement with lhaf_brute/lhaf_et
+  fds_terms         the same routine over a batch (pinned: equality with fds_term)
+  fds_range         pinned: fds_range(0, T) 2^{-n} = lhaf_fds = lhaf_brute, additivity over a
+                    split of [0, T), halving 2 sum_{t < T/2} = sum_{t < T}  (test_oracle_pins.py)
   lhaf_fds          pinned: agreement with lhaf_brute / lhaf_et, closed forms
   gbs_prob          pinned: squeezed-vacuum, coherent (Poisson) and thermal (geometric)
                     photon statistics, the sum rule sum_n P(n) = 1   (tests/test_gbs_pins.py)
@@ -62,6 +65,8 @@ def _load():
         lib.orc_matched_reps.restype = ctypes.c_int32
         lib.orc_fds_term.argtypes = [ctypes.c_int32, dp, dp, ip, ctypes.c_int32, dp]
         lib.orc_fds_term.restype = None
+        lib.orc_fds_terms.argtypes = [ctypes.c_int32, dp, dp, ip, ctypes.c_int32, ctypes.c_int32, dp]
+        lib.orc_fds_terms.restype = None
         lib.orc_lhaf_fds.argtypes = [dp, dp, ip, ctypes.c_int32, ctypes.c_int32, dp, dp]
         lib.orc_lhaf_fds.restype = ctypes.c_uint64
         _lib = lib
@@ -166,6 +171,19 @@ def fds_term(C, v, w, n: int) -> complex:
     out = np.zeros(2)
     _load().orc_fds_term(h, _dptr(C), _dptr(v), _iptr(w), n, _dptr(out))
     return complex(out[0], out[1])
+
+
+def fds_terms(C, v, W, n: int) -> np.ndarray:
+    """A batch of sieve terms g(w), one per row of W (nt x h), by the same explicit-power
+    routine as fds_term (OpenMP over the rows).  Parity status: pinned through fds_term."""
+    C = _cplx(C)
+    v = _cplx(v)
+    W = np.ascontiguousarray(np.atleast_2d(np.asarray(W, dtype=np.int32)))
+    nt, h = W.shape
+    assert C.shape == (2 * h, 2 * h) and v.shape == (2 * h,)
+    out = np.zeros(2 * nt)
+    _load().orc_fds_terms(h, _dptr(C), _dptr(v), _iptr(W), nt, n, _dptr(out))
+    return out[0::2] + 1j * out[1::2]
 
 
 def lhaf_fds(A, gamma, reps, mixed: bool = False):

@@ -331,6 +331,24 @@ void orc_fds_term(int32_t h, const double *C, const double *v, const int32_t *w,
   free(Cl); free(vl);
 }
 
+/* A batch of sieve terms (the same g(w) as orc_fds_term, one per row of w: nt x h int32),
+ * OpenMP over the terms.  A plain map of fds_term_ld, used by the per-term parity test (P14). */
+void orc_fds_terms(int32_t h, const double *C, const double *v, const int32_t *w, int32_t nt,
+                   int32_t n, double *out) {
+  int dim = 2 * h;
+  cld *Cl = (cld *)malloc(sizeof(cld) * (dim * dim > 0 ? dim * dim : 1));
+  cld *vl = (cld *)malloc(sizeof(cld) * (dim > 0 ? dim : 1));
+  for (int i = 0; i < dim * dim; ++i) Cl[i] = (long double)C[2 * i] + I * (long double)C[2 * i + 1];
+  for (int i = 0; i < dim; ++i) vl[i] = (long double)v[2 * i] + I * (long double)v[2 * i + 1];
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int32_t i = 0; i < nt; ++i) {
+    cld g = fds_term_ld(h, Cl, vl, w + (size_t)i * h, n);
+    out[2 * (size_t)i] = (double)creall(g);
+    out[2 * (size_t)i + 1] = (double)cimagl(g);
+  }
+  free(Cl); free(vl);
+}
+
 /* ------------------------------------------------------------------------- */
 /* Reduced matrix for a matching (reading C8): index list r = (p_1..p_H, q_1..q_H);
  * C_ab = A_{r_a r_b} including a = b (A's own diagonal = the weight of pairing two photons

@@ -83,6 +83,8 @@ def _load() -> ctypes.CDLL:
         "lhaf_job_reset": ([vp, vp]),
         "lhaf_job_run": ([vp, u64, u64, vp]),
         "lhaf_job_allreduce": ([vp, vp]),
+        "lhaf_job_reset_range": ([vp, u64, u64, vp]),
+        "lhaf_job_allreduce_range": ([vp, u64, u64, vp]),
         "lhaf_job_finalize": ([vp, vp, ctypes.c_int32, vp]),
         "lhaf_job_abs_sum": ([vp, dp]),
         "lhaf_job_partials": ([vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]),
@@ -130,12 +132,13 @@ def reload_library():
     _lib = _load()
     return _lib
 
-# every symbol include/lhaf.h declares (checked by tests/test_capi.py)
+# every symbol include/lhaf.h declares (checked by tests/test_host.py::test_library_exports_every_declared_symbol)
 EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed", "lhaf_rpt_cutoff",
             "lhaf_gbs_matrices", "lhaf_gbs_prob", "lhaf_ips_prob", "lhaf_rpt_et",
             "lhaf_rpt_multigamma",
             "lhaf_rpt_batch_dev", "lhaf_job_create", "lhaf_job_info_get", "lhaf_job_reset",
-            "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_finalize", "lhaf_job_abs_sum",
+            "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_reset_range", "lhaf_job_allreduce_range",
+            "lhaf_job_finalize", "lhaf_job_abs_sum",
             "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
             "lhaf_get_unique_id", "lhaf_init_rank", "lhaf_rank_info", "lhaf_set_kernel",
             "lhaf_shard_units", "lhaf_last_error", "lhaf_version", "lhaf_shutdown"]
@@ -307,6 +310,12 @@ class Job:
 
     def allreduce(self, stream: int = 0):
         _check(_lib.lhaf_job_allreduce(self._h, ctypes.c_void_p(stream)))
+
+    def reset_range(self, unit_begin: int, unit_end: int, stream: int = 0):
+        _check(_lib.lhaf_job_reset_range(self._h, unit_begin, unit_end, ctypes.c_void_p(stream)))
+
+    def allreduce_range(self, unit_begin: int, unit_end: int, stream: int = 0):
+        _check(_lib.lhaf_job_allreduce_range(self._h, unit_begin, unit_end, ctypes.c_void_p(stream)))
 
     def finalize(self, stream: int = 0) -> np.ndarray:
         out = np.zeros(2 * self.info.batch)

@@ -50,11 +50,15 @@ __device__ __forceinline__ double rcp_nr(double x) {
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
 }
-// 1/a = conj(a) / |a|^2 (pivots are O(1) up to the partial-pivoting growth: |a|^2 neither
-// over- nor underflows for the matrices this library accepts)
+// 1/a = conj(b) / |b|^2 * s with b = a s, s = 2^-floor(log2 max(|re|, |im|)) (exact): scale-free,
+// so a pivot anywhere in the normal range (1e-300 as well as 1e300) has a finite reciprocal
 __device__ __forceinline__ double2 crecip(double2 a) {
-  const double r = rcp_nr(fma(a.x, a.x, a.y * a.y));
-  return make_double2(a.x * r, -a.y * r);
+  const double m = fmax(fabs(a.x), fabs(a.y));
+  const int e = min((__double2hiint(m) >> 20) & 0x7ff, 2045);  // biased exponent of m
+  const double s = __hiloint2double((2046 - e) << 20, 0);      // 2^{-(e - 1023)}
+  const double bx = a.x * s, by = a.y * s;                      // max(|bx|, |by|) in [1, 2)
+  const double r = rcp_nr(fma(bx, bx, by * by)) * s;
+  return make_double2(bx * r, -by * r);
 }
 
 __device__ __forceinline__ double2 shfl2(double2 v, int src) {
@@ -77,6 +81,17 @@ __device__ __forceinline__ double2 warp_sum2(double2 v) {
     v.y += __shfl_xor_sync(LHAF_FULL, v.y, m);
   }
   return v;
+}
+
+// Pivot key of a candidate row (partial pivoting by |re| + |im|): the high word of the
+// double |re| + |im| (monotone for non-negative doubles; 11 exponent + 14 mantissa bits kept,
+// so the comparison is scale-free down to the smallest normal doubles -- a float conversion
+// would flush candidates below ~1e-38 to "zero"), plus 1 so that only an exact zero (or a
+// subnormal below 2^-1036) keeps the high part at 1 ("no pivot"), and the low 6 bits
+// = 63 - label so that ties go to the smallest label.  One REDUX.MAX per warp finds the pivot.
+__device__ __forceinline__ unsigned pivot_key(double2 v, int label) {
+  const unsigned hi = (unsigned)__double2hiint(fabs(v.x) + fabs(v.y));
+  return (((hi >> 6) + 1u) << 6) | (unsigned)(63 - label);
 }
 
 // ---------------------------------------------------------------- double-double

@@ -249,7 +249,7 @@ int lhaf::set_error(int status, const char *msg) {
 // ------------------------------------------------------------------ job
 struct lhaf_job {
   int batch = 0, kdim = 0, d_max = 0, n_max = 0, variant = 1;
-  int e_max = 0, ntl_max = 0;   // v2: bordered dimension and leading coefficients
+  int e_max = 0, ntl_max = 0;   // bordered dimension E and leading coefficients NTL
   bool any_loop = false;
   uint64_t units = 0, terms = 0, plan_bytes = 0;
   uint64_t parts = 0;  // partial records (= units, except cutoff groups: (eta_b + 1) per unit)
@@ -303,12 +303,23 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   const int kdim = mixed ? 2 * k : k;
   if (gamma_stride != 0 && gamma_stride < kdim)
     return fail(LHAF_E_ARG, "gamma_stride %lld < row length %d", (long long)gamma_stride, kdim);
-  if (!on_device) {
-    lhaf_status s = check_symmetric(A, kdim);
-    if (s != LHAF_OK) return s;
-  }
   lhaf_status s = ensure_device();
   if (s != LHAF_OK) return s;
+  if (on_device) {
+    // device inputs may have been written on any stream of the caller (e.g. a torch side
+    // stream): order every read below after them
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (kdim <= 2048) {  // the same symmetry / finiteness check as for host inputs
+      std::vector<double> acopy(2 * std::max<size_t>(1, (size_t)kdim * kdim));
+      if (kdim > 0)
+        CUDA_TRY(cudaMemcpy(acopy.data(), A, (size_t)kdim * kdim * 16, cudaMemcpyDeviceToHost));
+      s = check_symmetric(acopy.data(), kdim);
+      if (s != LHAF_OK) return s;
+    }
+  } else {
+    s = check_symmetric(A, kdim);
+    if (s != LHAF_OK) return s;
+  }
 
   // host view of gamma (loop flags are planned on the host)
   const size_t gamma_len = gamma_stride ? (size_t)batch * gamma_stride : (size_t)kdim;
@@ -413,7 +424,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     uint64_t R = 1;
     for (int h = 0; h < P.H; ++h) { upool.push_back(R); R *= (uint64_t)(P.eta[h] + 1); }
     D.mat_off = cpool_words;
-    cpool_words += (int64_t)(P.d + 1) * (P.d + 1) + 2 * P.d + 2;  // v1: Ct|uh|v|beta; v2: E x E
+    cpool_words += (int64_t)(P.d + 1) * (P.d + 1) + 2 * P.d + 2;  // v1: Ct|uh|v|beta; v3/v5: E x E
   }
   j->units = unit;
   j->parts = part;
@@ -443,8 +454,8 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       e = cudaMemcpy(j->d_gamma, gamma, gamma_len * sizeof(double2), cudaMemcpyHostToDevice);
   }
   j->variant = g_ctx.variant ? g_ctx.variant : choose_variant(j->e_max, j->n_max);
-  if (j->variant >= 2 && !v2_supported(j->e_max, j->n_max)) j->variant = 1;
-  if (e == cudaSuccess) e = (j->variant >= 2) ? launch_prep_v2(j->dev(), 0) : launch_prep(j->dev(), j->d_max, 0);
+  if (j->variant >= 3 && !bordered_supported(j->e_max, j->n_max)) j->variant = 1;
+  if (e == cudaSuccess) e = (j->variant >= 3) ? launch_prep_bordered(j->dev(), 0) : launch_prep(j->dev(), j->d_max, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     job_free(j);
@@ -457,8 +468,6 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
 static cudaError_t run_sieve(lhaf_job *j, uint64_t b, uint64_t e, cudaStream_t st) {
   if (j->variant == 3)
     return launch_sieve_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st);
-  if (j->variant == 2)
-    return launch_sieve_v2(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st);
   return launch_sieve(j->dev(), j->variant, j->d_max, j->n_max, b, e, g_ctx.num_sms, st);
 }
 
@@ -473,7 +482,10 @@ static void rank_units(uint64_t units, uint64_t &b, uint64_t &e) {
 }
 
 static lhaf_status job_allreduce_impl(lhaf_job *j, cudaStream_t st) {
-  if (g_ctx.nranks <= 1 || j->units == 0) return LHAF_OK;
+  // no communicator: a single rank without NCCL (nothing to exchange); a 1-rank communicator
+  // (lhaf_init_rank(0, 1, id, dev) with an id) runs the same ncclAllReduce as N ranks do
+  if (!g_ctx.comm && g_ctx.nranks <= 1) return LHAF_OK;
+  if (j->units == 0) return LHAF_OK;
   if (!g_ctx.comm) return fail(LHAF_E_STATE, "multi-rank all-reduce without a communicator");
   const size_t count = (size_t)j->units * (sizeof(Partial) / sizeof(double));
   ncclResult_t r = g_ctx.nccl.AllReduce(j->d_partials, j->d_partials, count, ncclDouble, ncclSum,
@@ -549,7 +561,8 @@ lhaf_status lhaf_set_device(int32_t device) {
 }
 
 lhaf_status lhaf_set_kernel(int32_t variant) {
-  if (variant < 0 || variant > 3) return fail(LHAF_E_ARG, "unknown kernel variant %d", variant);
+  if (variant < 0 || variant > 3 || variant == 2)
+    return fail(LHAF_E_ARG, "unknown kernel variant %d (0 = default, 1 = Householder, 3 = v3)", variant);
   g_ctx.variant = variant;
   return LHAF_OK;
 }
@@ -571,7 +584,6 @@ lhaf_status lhaf_job_info_get(const lhaf_job *j, lhaf_job_info *info) {
     if (D.d > 0) {
       const bool lp = (D.flags & FLAG_LOOP) != 0;
       info->flops_per_term_model = (j->variant == 3)   ? v3_flops_per_term(D.d, D.n, lp)
-                                   : (j->variant == 2) ? v2_flops_per_term(D.d, D.n, lp)
                                                        : flops_per_term(j->variant, D.d, D.n, true);
       break;
     }
@@ -582,6 +594,28 @@ lhaf_status lhaf_job_reset(lhaf_job *j, void *stream) {
   if (!j) return fail(LHAF_E_ARG, "null job");
   CUDA_TRY(cudaMemsetAsync(j->d_partials, 0, std::max<uint64_t>(1, j->units) * sizeof(Partial),
                            (cudaStream_t)stream));
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_reset_range(lhaf_job *j, uint64_t ub, uint64_t ue, void *stream) {
+  if (!j) return fail(LHAF_E_ARG, "null job");
+  if (ue > j->units || ub > ue) return fail(LHAF_E_ARG, "unit range outside the job");
+  if (ue > ub)
+    CUDA_TRY(cudaMemsetAsync(j->d_partials + ub, 0, (ue - ub) * sizeof(Partial), (cudaStream_t)stream));
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_allreduce_range(lhaf_job *j, uint64_t ub, uint64_t ue, void *stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!j) return fail(LHAF_E_ARG, "null job");
+  if (ue > j->units || ub > ue) return fail(LHAF_E_ARG, "unit range outside the job");
+  if (!g_ctx.comm && g_ctx.nranks <= 1) return LHAF_OK;
+  if (ue == ub) return LHAF_OK;
+  if (!g_ctx.comm) return fail(LHAF_E_STATE, "multi-rank all-reduce without a communicator");
+  const size_t count = (size_t)(ue - ub) * (sizeof(Partial) / sizeof(double));
+  ncclResult_t r = g_ctx.nccl.AllReduce(j->d_partials + ub, j->d_partials + ub, count, ncclDouble,
+                                        ncclSum, g_ctx.comm, (cudaStream_t)stream);
+  if (r != ncclSuccess) return fail(LHAF_E_NCCL, "ncclAllReduce: %s", g_ctx.nccl.GetErrorString(r));
   return LHAF_OK;
 }
 
@@ -642,7 +676,6 @@ lhaf_status lhaf_job_terms(lhaf_job *j, const uint64_t *t, int32_t nt, double *g
   if (e == cudaSuccess) {
     const PatDesc &D0 = j->descs[0];
     e = (j->variant == 3)   ? launch_terms_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
-        : (j->variant == 2) ? launch_terms_v2(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
                             : launch_terms(j->dev(), j->variant, D0.d, D0.n, dt, nt, dg, 0);
   }
   if (e == cudaSuccess) e = cudaMemcpy(g_out, dg, nt * sizeof(double2), cudaMemcpyDeviceToHost);
@@ -701,13 +734,20 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
       }
       int nf = 0;
       uint64_t Tf = 1;
-      for (int e2 : G.eta) { nf += e2; Tf *= (uint64_t)(e2 + 1); }
+      for (int e2 : G.eta) {
+        nf += e2;
+        const uint64_t r = (uint64_t)e2 + 1;
+        if (Tf > (~(uint64_t)0) / r) return fail(LHAF_E_TOO_LARGE, "cutoff term count overflows 64 bits");
+        Tf *= r;
+      }
       G.p.push_back(mode); G.q.push_back(mode); G.eta.push_back(2 * G.eta_b);  // digit range
       G.H = (int)G.eta.size();
       G.d = 2 * G.H;
       G.n = nf + G.eta_b;
       G.N = Pf.N + par;
-      G.T = Tf * (uint64_t)(2 * G.eta_b + 1);
+      const uint64_t rb = (uint64_t)(2 * G.eta_b + 1);
+      if (Tf > (~(uint64_t)0) / rb) return fail(LHAF_E_TOO_LARGE, "cutoff term count overflows 64 bits");
+      G.T = Tf * rb;
       G.T_eval = G.T / 2;
       n_f[par] = nf;
       gidx[par] = (int)groups.size();
@@ -716,7 +756,9 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
   }
   lhaf_job *j = nullptr;
   if (shared) s = job_create_impl(A, gamma, 0, nullptr, k, (int)groups.size(), 0, false, &j, &groups);
-  if (!shared || (s == LHAF_OK && j->variant != 3)) {
+  // the shared groups carry the batched self-pair (and a phantom for odd counts), so they can
+  // exceed the kernels' d limit where every per-count pattern still fits: fall back then too
+  if (!shared || (s == LHAF_OK && j->variant != 3) || s == LHAF_E_TOO_LARGE) {
     if (j) { job_free(j); j = nullptr; }
     std::vector<int32_t> reps((size_t)(n_cut + 1) * k);  // separate sieve per count
     for (int c = 0; c <= n_cut; ++c) {
@@ -846,7 +888,7 @@ lhaf_status lhaf_init_rank(int32_t rank, int32_t nranks, const void *id128, int3
   if (g_ctx.comm) { g_ctx.nccl.CommDestroy(g_ctx.comm); g_ctx.comm = nullptr; }
   g_ctx.rank = rank;
   g_ctx.nranks = nranks;
-  if (nranks == 1) return LHAF_OK;
+  if (nranks == 1 && !id128) return LHAF_OK;  // single rank without NCCL
   if (!id128) return fail(LHAF_E_ARG, "null unique id");
   if (!g_ctx.nccl.load()) return fail(LHAF_E_NCCL, "cannot dlopen libnccl.so.2");
   ncclUniqueId id;

@@ -68,18 +68,13 @@ cudaError_t launch_terms(const JobDev &job, int variant, int d_max, int n_max, c
 double flops_per_term(int variant, int d, int n, bool loops);
 int choose_variant(int d_max, int n_max);
 
-// Variant 2 (lhaf_v2.cu): register-resident Gauss-transform Hessenberg of the bordered matrix.
+// The bordered column-swapped matrix B0 of every pattern (prep of variants 3 and 5).
 // e_max = max over patterns of d + (loops ? 1 : 0); ntl_max = max of min(n + (loops ? 2 : 1), E + 1).
-int v2_supported(int e_max, int n_max);
-cudaError_t launch_prep_v2(const JobDev &job, cudaStream_t s);
-cudaError_t launch_sieve_v2(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t unit_begin,
-                            uint64_t unit_end, int num_sms, cudaStream_t s);
-cudaError_t launch_terms_v2(const JobDev &job, int e, int ntl, int n, const uint64_t *t, int nt,
-                            double2 *g_out, cudaStream_t s);
-double v2_flops_per_term(int d, int n, bool loops);
+int bordered_supported(int e_max, int n_max);
+cudaError_t launch_prep_bordered(const JobDev &job, cudaStream_t s);
 
 // Variant 3 (lhaf_v3.cu): branch-free fused per-column body, band + trailing La Budde.
-// Uses the v2 prep kernel (bordered column-swapped B0).
+// Uses the bordered column-swapped B0 of launch_prep_bordered.
 cudaError_t launch_sieve_v3(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t unit_begin,
                             uint64_t unit_end, int num_sms, cudaStream_t s);
 // cutoff groups (FLAG_CUT patterns): one term serves every count of the batched mode

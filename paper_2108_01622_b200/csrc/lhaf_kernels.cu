@@ -344,6 +344,39 @@ __global__ void __launch_bounds__(128) prep_kernel(JobDev J) {
   }
 }
 
+// ================================================================ prep of the bordered matrix (a3)
+// One warp per pattern.  Reduced system (reading C8): C_ab = A[r_a][r_b] (phantom rows and
+// columns zero), v_a = gamma[r_a] (phantom 1).  Stores the column-swapped bordered matrix
+// B0 = [[0, (v X)^T], [v, C X]] (E = d + 1) when loop terms are present, else B0 = C X
+// (E = d); X swaps the two halves of the index list.  Per term B = B0 diag(1, w, w).
+__global__ void __launch_bounds__(128) prep_bordered(JobDev J) {
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= J.npat) return;
+  const PatDesc P = J.descs[p];
+  const int d = P.d;
+  if (d == 0) return;
+  const int H = P.H;
+  const int o = (P.flags & FLAG_LOOP) ? 1 : 0;
+  const int E = d + o;
+  const int *r = J.ipool + P.idx_off;
+  double2 *B0 = J.cpool + P.mat_off;
+  const double2 *g = J.gamma + P.gamma_off;
+  for (int idx = lane; idx < E * E; idx += 32) {
+    const int a = idx / E - o, c = idx % E - o;          // reduced indices, -1 = border
+    const int b = c < 0 ? -1 : (c < H ? c + H : c - H);  // partner column
+    double2 x = c0();
+    if (a >= 0 && c >= 0) {
+      x = (r[a] < 0 || r[b] < 0) ? c0() : J.A[(size_t)r[a] * J.kdim + r[b]];
+    } else if (a < 0 && c >= 0) {
+      x = (r[b] < 0) ? c1() : g[r[b]];
+    } else if (a >= 0 && c < 0) {
+      x = (r[a] < 0) ? c1() : g[r[a]];
+    }
+    B0[idx] = x;
+  }
+}
+
 // ================================================================ finalize (a11-a12)
 // One block per pattern: thread i double-double-sums the contiguous unit range
 // [i c, (i+1) c) in order, then thread 0 adds the 128 thread sums in order.  The order
@@ -423,6 +456,12 @@ cudaError_t launch_sieve(const JobDev &job, int variant, int dmax, int nmax, uin
   return cudaGetLastError();
 }
 
+cudaError_t launch_prep_bordered(const JobDev &job, cudaStream_t s) {
+  if (job.npat == 0) return cudaSuccess;
+  prep_bordered<<<(job.npat + 3) / 4, 128, 0, s>>>(job);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_finalize(const JobDev &job, double2 *out, double *abs_out, cudaStream_t s) {
   if (job.npat == 0) return cudaSuccess;
   finalize_kernel<<<job.npat, 128, 0, s>>>(job, out, abs_out);
@@ -461,6 +500,7 @@ double flops_per_term(int variant, int d, int n, bool loops) {
   return 8.0 * cmac;
 }
 
-int choose_variant(int e_max, int n_max) { return v2_supported(e_max, n_max) ? 3 : 1; }
+int bordered_supported(int e_max, int n_max) { return e_max <= 64 && n_max + 2 <= 255; }
+int choose_variant(int e_max, int n_max) { return bordered_supported(e_max, n_max) ? 3 : 1; }
 
 }  // namespace lhaf

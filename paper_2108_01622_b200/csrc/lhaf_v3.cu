@@ -534,11 +534,7 @@ __device__ __forceinline__ void phase_steps(double2 (&A)[CSP], PhaseSt &st, int 
     st.buf ^= 1;
     LHAF_SP(0)
     const bool candr = st.label > k && st.label < E;
-    unsigned key = 0u;
-    if (candr) {
-      const unsigned fbits = __float_as_uint((float)(fabs(st.colv.x) + fabs(st.colv.y)));
-      key = (((fbits >> 6) + 1u) << 6) | (unsigned)(63 - st.label);
-    }
+    const unsigned key = candr ? pivot_key(st.colv, st.label) : 0u;
     const unsigned wkey = __reduce_max_sync(LHAF_FULL, key);
     LHAF_SP(1)
     if (par == 0 && st.mypos >= 0) kb[st.mypos] = candr ? st.colv : c0();
@@ -803,11 +799,7 @@ __device__ __forceinline__ void team_reduce(const PatDesc &P, const Pattern &D, 
     const bool candr = label > k && label < E;
     // pivot key: |re| + |im| as a float (monotone bits), low 6 bits = 63 - label so that ties
     // go to the smallest label; non-candidates 0; one REDUX per warp
-    unsigned key = 0u;
-    if (candr) {
-      const unsigned fbits = __float_as_uint((float)(fabs(colv.x) + fabs(colv.y)));
-      key = (((fbits >> 6) + 1u) << 6) | (unsigned)(63 - label);
-    }
+    const unsigned key = candr ? pivot_key(colv, label) : 0u;
     const unsigned wkey = __reduce_max_sync(LHAF_FULL, key);
     if (par == 0) kb[rr] = candr ? colv : c0();
     if (candr && key == wkey) {  // this warp's best row publishes itself (and 1 / its pivot)
@@ -1081,140 +1073,6 @@ sieve_cut_v3(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
   }
 }
 
-// ================================================================ v4: reduction teams + tail warp
-// La Budde + series of one term in one warp (a7-a9) from a band hb written by a team; Q and
-// the series scratch are the warp's own.
-__device__ __forceinline__ double2 warp_tail(const double2 *hb, double2 *Q, const Pattern &D,
-                                             int lane) {
-  const int n = D.n, E = D.E, NTL = D.NTL;
-#ifdef LHAF_V4_NOTAIL  // diagnostic: the reduction teams' throughput alone
-  return c0();
-#endif
-  if (NTL <= 32) labudde<1>(hb, Q, E, NTL, lane);
-  else labudde<2>(hb, Q, E, NTL, lane);
-  const double2 *cB = Q;
-  const double2 *cM = D.loops ? Q + NTL : Q;
-  double2 *scr = Q + (E + 1) * NTL;
-  if (n + 2 <= 32) return series<1>(cM, cB, n, NTL, D.loops, scr, lane);
-  if (n + 2 <= 64) return series<2>(cM, cB, n, NTL, D.loops, scr, lane);
-  return series<5>(cM, cB, n, NTL, D.loops, scr, lane);
-}
-
-__device__ __forceinline__ void nb_sync(int id, int cnt) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void nb_arrive(int id, int cnt) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
-}
-
-// Two reduction teams and one tail warpgroup per CTA (NW = 4).  Team t reduces the unit's
-// terms tb+t, tb+t+2, ... into its two band buffers in turn; tail warp t takes team t's bands
-// in order (single-warp La Budde, series, accumulation) while the team reduces the next term,
-// so the reduction is the only work on the teams' critical path.  setmaxnreg moves registers
-// from the tail warpgroup (RA) to the reduction warpgroups (RT): the launch gives every warp
-// 168 (3 warps per SM sub-partition) and 2 RT + RA <= 3 * 168.  Named barriers hand a buffer
-// over: FULL(t, b) = 3 + 2t + b (team arrives, tail warp syncs), EMPTY(t, b) = 7 + 2t + b
-// (tail warp arrives, team syncs before refilling b); 1 and 2 are the teams' own, 12 brackets
-// the unit fetch, 13 joins the two tail warps' sums.
-template <int S, int CS, int RT, int RA, bool CMP>
-__global__ void __launch_bounds__(384, 1)
-sieve_v4(JobDev J, uint64_t ubeg, uint64_t uend, int team_words, int aux_words) {
-  constexpr int NW = 4;
-  using Sh = Shape<S, CS, NW>;
-  static_assert(2 * RT + RA <= 3 * 168, "register budget");
-  extern __shared__ double2 smem[];
-  __shared__ unsigned long long s_unit;
-  __shared__ double2 s_hand[2][2];  // (sign * weight, weight) per team and buffer
-  __shared__ double s_acc[6];
-  constexpr int TS = 32 * NW, NT = 3 * TS, HAND = TS + 32;
-  const int wg = threadIdx.x / TS, tid = threadIdx.x % TS;
-  const int warp = tid >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 2 * team_words + aux_words; i += NT) smem[i] = c0();
-  double2 *abase = smem + 2 * (size_t)team_words;
-  // the two roles run separate loops (so that each is compiled under its own register budget);
-  // barrier 12 (whole CTA) brackets the unit fetch
-  if (wg < 2) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(RT));
-    const int team = wg;
-    double2 *base = smem + (size_t)team * team_words;
-    for (;;) {
-      nb_sync(12, NT);
-      if (threadIdx.x == 0) s_unit = ubeg + atomicAdd(J.counter, 1ull);
-      nb_sync(12, NT);
-      const uint64_t u = s_unit;
-      if (u >= uend) break;
-      const PatDesc P = J.descs[find_pattern(J, u)];
-      const Pattern D = pattern_of(P);
-      const uint64_t tb = (u - P.unit_begin) * P.chunk;
-      const uint64_t te = min(tb + P.chunk, P.T_eval);
-      const int EN = D.E * D.NTL;
-      TeamMem T;
-      T.u1 = base + 2 * EN;
-      T.wv = reinterpret_cast<int *>(T.u1 + Sh::red_words());
-      T.ww = reinterpret_cast<double *>(T.u1 + Sh::red_words() + 32);
-      int use = 0;
-      for (uint64_t t = tb + team; t < te; t += 2, ++use) {
-        const int b = use & 1;
-        if (use >= 2) nb_sync(7 + 2 * team + b, HAND);
-        T.hb = base + b * EN;
-        int sign = 1;
-        double weight = 1.0;
-#ifndef LHAF_V4_NOTEAM  // diagnostic: the tail warps' throughput alone (bands of zeros)
-        team_reduce<S, CS, NW, 2, CMP>(P, D, J, t, T, tid, team, sign, weight);
-#endif
-        if (tid == 0) s_hand[team][b] = make_double2(sign * weight, weight);
-        nb_arrive(3 + 2 * team + b, HAND);
-      }
-    }
-  } else {
-    // tail warps 0 and 1 serve teams 0 and 1 (single-warp La Budde + series, in term order);
-    // warps 2 and 3 only keep the unit barrier
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(RA));
-    for (;;) {
-      nb_sync(12, NT);
-      nb_sync(12, NT);
-      const uint64_t u = s_unit;
-      if (u >= uend) break;
-      if (warp >= 2) continue;
-      const PatDesc P = J.descs[find_pattern(J, u)];
-      const Pattern D = pattern_of(P);
-      const uint64_t tb = (u - P.unit_begin) * P.chunk;
-      const uint64_t te = min(tb + P.chunk, P.T_eval);
-      const int nterm = (int)(te - tb);
-      const int EN = D.E * D.NTL;
-      const int team = warp, nt = (nterm - team + 1) / 2;
-      double2 *Q = abase + (size_t)team * (aux_words / 2);
-      double rh = 0, rl = 0, ih = 0, il = 0, ah = 0, al = 0;
-      for (int use = 0; use < nt; ++use) {
-        const int b = use & 1;
-        nb_sync(3 + 2 * team + b, HAND);
-        const double2 g = warp_tail(smem + (size_t)team * team_words + b * EN, Q, D, lane);
-        const double2 hw = s_hand[team][b];
-        __syncwarp();
-        if (use + 2 < nt) nb_arrive(7 + 2 * team + b, HAND);
-        if (lane == 0) {
-          dd_add(rh, rl, hw.x * g.x);
-          dd_add(ih, il, hw.x * g.y);
-          dd_add(ah, al, hw.y * hypot(g.x, g.y));
-        }
-      }
-      if (team == 1 && lane == 0) {
-        s_acc[0] = rh; s_acc[1] = rl; s_acc[2] = ih; s_acc[3] = il; s_acc[4] = ah; s_acc[5] = al;
-      }
-      nb_sync(13, 64);
-      if (team == 0 && lane == 0) {
-        dd_add_dd(rh, rl, s_acc[0], s_acc[1]);
-        dd_add_dd(ih, il, s_acc[2], s_acc[3]);
-        dd_add_dd(ah, al, s_acc[4], s_acc[5]);
-        Partial q;
-        q.re_hi = rh; q.re_lo = rl; q.im_hi = ih; q.im_lo = il; q.abs_hi = ah; q.abs_lo = al;
-        q.pad0 = 0; q.pad1 = 0;
-        J.partials[u] = q;
-      }
-    }
-  }
-}
-
 // g(t) (unweighted) of pattern 0 for a list of term indices; one team per index.
 template <int S, int CS, int NW, int TEAMS, int REGS, bool CMP>
 __global__ void __maxnreg__(REGS)
@@ -1302,42 +1160,6 @@ struct Inst {
   }
 };
 
-template <int S, int CS, int RT, int RA, bool CMP>
-struct Inst4 {
-  static constexpr int NW = 4;
-  using Sh = Shape<S, CS, NW>;
-  static constexpr int EMAX = Sh::EMAX;
-  static constexpr int THREADS = 3 * 32 * NW;
-  static cudaError_t sieve(const JobDev &job, int E, int NTL, int n, uint64_t ubeg, uint64_t uend,
-                           int num_sms, cudaStream_t s) {
-    const int tw = 2 * E * NTL + Sh::red_words() + 64;
-    const int aw = 2 * ((E + 1) * NTL + 3 * (n + 2));
-    const size_t smem = (size_t)(2 * tw + aw) * sizeof(double2);
-    auto *kern = sieve_v4<S, CS, RT, RA, CMP>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
-    if (e != cudaSuccess) return e;
-    if (getenv("LHAF_DEBUG_V4")) {
-      cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, kern);
-      fprintf(stderr, "v4: E=%d NTL=%d smem=%zu per_sm=%d regs=%d maxthreads=%d\n", E, NTL, smem, per_sm,
-              fa.numRegs, fa.maxThreadsPerBlock);
-    }
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const uint64_t units = uend - ubeg;
-    uint64_t grid = (uint64_t)num_sms * per_sm;
-    if (grid > units) grid = units;
-    e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return e;
-    kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw, aw);
-    return cudaGetLastError();
-  }
-};
-
 // <S, CS, NW, TEAMS, registers per thread>.  Each SM sub-partition has 16K registers, so a
 // warp of R registers allows floor(512 / R) warps per sub-partition.
 using I9 = Inst<1, 9, 1, 4, 128>;
@@ -1347,21 +1169,11 @@ using I32 = Inst<1, 32, 1, 4, 168, true>;
 using I48 = Inst<2, 24, 3, 1, 168, true>;
 using I62 = Inst<2, 31, 4, 1, 232, true>;  // 2 CTAs / SM (2 warps per 16K-register sub-partition)
 using I64 = Inst<2, 32, 4, 1, 168, true>;
-// alternatives (LHAF_V3_ALT=1): more lanes per row, fewer registers, more warps per SM
-using A26 = Inst<2, 13, 2, 2, 104>;   // E <= 26: 4 warps / CTA
-using A48 = Inst<4, 12, 6, 1, 128, true>;   // E <= 48: 6 warps / CTA
-using A64 = Inst<4, 16, 8, 1, 128, true>;   // E <= 64: 8 warps / CTA
-// (LHAF_V3_ALT=3) single-phase reduction (no compaction)
+// (LHAF_V3_ALT=3) single-phase reduction (no compaction): a second rounding order of the same
+// method, kept for the accuracy cross-checks (tests/test_gpu_variants.py)
 using P25 = Inst<1, 25, 1, 4, 168>;
 using P48 = Inst<2, 24, 3, 1, 168>;
 using P62 = Inst<2, 31, 4, 1, 255>;
-// (LHAF_V3_ALT=5) phased reduction at 255 registers
-using R48 = Inst<2, 24, 3, 1, 255, true>;
-using R62 = Inst<2, 31, 4, 1, 255, true>;
-// (LHAF_V3_ALT=6) single-phase reduction at 168 registers: 3 CTAs / SM for E <= 62
-using T62 = Inst<2, 31, 4, 1, 168>;
-// (LHAF_V3_ALT=8) v4: two reduction teams + one tail warp per CTA
-using V62 = Inst4<2, 31, 208, 88, false>;  // (measured best of 232/40 .. 200/104)
 static int alt_mode() {
   static const int m = [] { const char *e = getenv("LHAF_V3_ALT"); return e ? atoi(e) : 0; }();
   return m;
@@ -1402,16 +1214,6 @@ extern "C" int lhaf_debug_phase_cycles(unsigned long long *out8) {
     if (E > 32 && E <= v3::P48::EMAX) return v3::P48::CALL; \
     if (E > 48 && E <= v3::P62::EMAX) return v3::P62::CALL; \
   }                                             \
-  if (v3::alt_mode() == 6 && E > 48 && E <= v3::T62::EMAX) return v3::T62::CALL; \
-  if (v3::alt_mode() == 5) {                    \
-    if (E > 32 && E <= v3::R48::EMAX) return v3::R48::CALL; \
-    if (E > 48 && E <= v3::R62::EMAX) return v3::R62::CALL; \
-  }                                             \
-  if (v3::alt_mode() == 1) {                    \
-    if (E <= v3::A26::EMAX && E > 17) return v3::A26::CALL; \
-    if (E <= v3::A48::EMAX && E > 32) return v3::A48::CALL; \
-    if (E <= v3::A64::EMAX && E > 48) return v3::A64::CALL; \
-  }                                             \
   if (E <= v3::I9::EMAX) return v3::I9::CALL;   \
   if (E <= v3::I17::EMAX) return v3::I17::CALL; \
   if (E <= v3::I25::EMAX) return v3::I25::CALL; \
@@ -1427,8 +1229,6 @@ cudaError_t launch_sieve_v3(const JobDev &job, int e_max, int ntl_max, int n_max
   cudaError_t e = v3::ensure_inv();
   if (e != cudaSuccess) return e;
   const int E = e_max;
-  if (v3::alt_mode() == 8 && E > 48 && E <= v3::V62::EMAX)
-    return v3::V62::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
   LHAF_V3_DISPATCH(sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s))
 }
 

@@ -107,3 +107,66 @@ def test_shard_units_partition_many_ranks(lib):
                 assert b == prev and e >= b
                 prev = e
             assert prev == units
+
+
+class _GlooJob:
+    """Stand-in for paper_2108_01622_b200.Job with bench.py's per-step calls, on CPU: the
+    "kernel" writes each unit's partial (overwriting, as the sieve does), the range all-reduce
+    is a gloo all_reduce of that slice, finalize is the ordered double-double sum."""
+
+    def __init__(self, units):
+        self.P = torch.zeros((units, 8), dtype=torch.float64)
+        self.out = None
+
+    def reset_range(self, b, e, stream=0):
+        self.P[b:e] = 0.0
+
+    def run(self, b, e, stream=0):
+        for u in range(b, e):
+            self.P[u] = torch.from_numpy(partial_value(u))
+
+    def allreduce_range(self, b, e, stream=0):
+        view = self.P[b:e].clone()
+        dist.all_reduce(view)
+        self.P[b:e] = view
+
+    def finalize_dev(self, out_ptr, stream=0):
+        self.out = dd_finalize(self.P.numpy())
+
+
+def _bench_worker(rank, world, port, units, slices, steps, q):
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    job = _GlooJob(units)
+    for s in range(steps):
+        bench.hot_path_step(job, s, units, slices, rank, world, 0, 0)
+    q.put((rank, job.out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("units,slices,steps", [(37, 1, 5), (300, 4, 9), (64, 64, 70)])
+def test_bench_step_protocol_two_ranks(units, slices, steps):
+    # bench.py's step (zero the slice, evaluate the rank's share, all-reduce the slice,
+    # finalize) over repeated slices: the 2-rank result equals the 1-rank result bit for bit
+    # and nothing is counted twice when a slice is evaluated again (ADVICE r1, bench.py:254)
+    import bench
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_bench_worker, args=(r, 2, port, units, slices, steps, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    covered = set()
+    for s in range(steps):
+        sb, se, _, _ = bench.slice_bounds(units, s, slices, 0, 1)
+        covered.update(range(sb, se))
+    P = np.zeros((units, 8))
+    for u in covered:
+        P[u] = partial_value(u)
+    want = dd_finalize(P)
+    assert res[0] == want and res[1] == want, (res, want)

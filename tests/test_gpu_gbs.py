@@ -54,17 +54,22 @@ def test_gbs_prob_textbook_statistics(lib):
         assert rel(lib.lhaf_gbs_prob(sig, al, [n]).real, want) <= 1e-12
 
 
-def test_gbs_sum_rule(lib):
-    # 3 modes, weak squeezing, loss and displacement: sum over |n| <= 6 approaches 1 (the
-    # oracle's tail beyond |n| = 6 is 1.14e-5)
+def test_gbs_sum_rule(lib, orc):
+    # 3 modes, weak squeezing, loss and displacement: the probabilities over |n| <= 6 sum to
+    # 1 minus the tail (P:317 normalisation; the tail beyond |n| = 6 is ~1.1e-5), and the
+    # partial sum equals the oracle's (explicit A_n, brute force) over the same patterns
     rng = G.rng_for(1555)
     U = G.haar_unitary(3, rng)
     sig, al = G.gaussian_state(U, [0.2, 0.15, 0.25], [0.9, 0.8, 0.85], [0.1, 0.1j, -0.05])
     tot = 0.0
+    tot_orc = 0.0
     for a in range(7):
         for b in range(7 - a):
             for c in range(7 - a - b):
                 tot += lib.lhaf_gbs_prob(sig, al, [a, b, c]).real
+                tot_orc += orc.gbs_prob(sig, al, [a, b, c]).real
+    assert 1.0 - 2e-5 < tot < 1.0, tot
+    assert abs(tot - tot_orc) <= 1e-12, (tot, tot_orc)
 
 
 

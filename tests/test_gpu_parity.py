@@ -3,8 +3,9 @@
 Tolerances (north_star, BASELINE.json): relative error <= 1e-10 for N <= 24 photons,
 <= 1e-8 for N <= 60; integer decode bit-exact (tests/test_host.py).  Where the exact value
 is 0 or tiny (odd N with gamma = 0), the comparison is absolute against the oracle's own
-sum |term| scale (reading C18).  Every oracle value used here is computed live by oracle/ or
-read from tests/golden/ (written by tools/make_golden.py, which calls only oracle/).
+sum |term| scale (reading C18).  Every oracle value used here is computed live by oracle/
+(the paper's printed values -- the worked example of P:133-135 -- sit in tests/golden/ with
+their citations and are used by the CPU pin tests).
 """
 import json
 import math
@@ -111,26 +112,36 @@ def test_batch_mixed_shapes(lib, orc):
         assert rel(v, ref) <= 1e-10, (p, v, ref)
 
 
-def test_per_term_parity(lib, orc):
-    # P14: g(t) on sampled t at d = 24, 48, 60 against the oracle's explicit-power term
-    cases = [(G.config(4), False), (G.config(5), True)]
-    c2 = G.config(2)
-    cases.append((dict(A=c2["A"], gamma=c2["gamma"], reps=c2["reps_batch"][0]), False))
-    for cfg, mixed in cases:
-        # mixed states are planned by the greedy matching of the doubled pattern (C11b)
-        reps_o = np.concatenate([cfg["reps"], cfg["reps"]]) if mixed else cfg["reps"]
-        C, v, eta, n = orc.reduced_system(cfg["A"], cfg["gamma"], reps_o, mixed=False)
-        info = lib.lhaf_plan(cfg["reps"], mixed=mixed)
-        assert info.etas() == eta and info.n == n
-        job = lib.Job(cfg["A"], cfg["gamma"], cfg["reps"], mixed=mixed)
-        rng = G.rng_for(99)
-        ts = rng.integers(0, info.T_eval, 12, dtype=np.uint64)
-        gg = job.terms_g(ts)
-        refs = [orc.fds_term(C, v, orc.decode(int(t), eta)[1], n) for t in ts]
-        scale = max(abs(r) for r in refs)
-        err = max(abs(a - b) for a, b in zip(gg, refs)) / scale
-        assert err <= 1e-10, (C.shape, err)   # mixed d = 48 terms: ~5e-11 (weights up to 3)
-        job.close()
+@pytest.mark.parametrize("which", ["cfg4_d60", "cfg5_d48", "cfg2_d24"])
+def test_per_term_parity(lib, orc, which):
+    # P14: g(t) on 1024 seeded sampled t at d = 60 (cfg4), 48 (cfg5, greedy matching of the
+    # doubled pattern, C11b) and 24 (a cfg2 pattern) against the oracle's explicit-power term
+    # (long double).  Reported: median and max of |g_gpu - g_ref| / |g_ref| per term and of
+    # |g_gpu - g_ref| / max_t |g_ref|; asserted: the latter <= 1e-10 for every sampled t.
+    if which == "cfg4_d60":
+        cfg, mixed = G.config(4), False
+    elif which == "cfg5_d48":
+        cfg, mixed = G.config(5), True
+    else:
+        c2 = G.config(2)
+        cfg, mixed = dict(A=c2["A"], gamma=c2["gamma"], reps=c2["reps_batch"][0]), False
+    reps_o = np.concatenate([cfg["reps"], cfg["reps"]]) if mixed else cfg["reps"]
+    C, v, eta, n = orc.reduced_system(cfg["A"], cfg["gamma"], reps_o, mixed=False)
+    info = lib.lhaf_plan(cfg["reps"], mixed=mixed)
+    assert info.etas() == eta and info.n == n
+    job = lib.Job(cfg["A"], cfg["gamma"], cfg["reps"], mixed=mixed)
+    rng = G.rng_for(99)
+    ts = rng.integers(0, info.T_eval, 1024, dtype=np.uint64)
+    gg = job.terms_g(ts)
+    job.close()
+    W = np.array([orc.decode(int(t), eta)[1] for t in ts], np.int32)
+    refs = orc.fds_terms(C, v, W, n)
+    scale = np.max(np.abs(refs))
+    err_abs = np.abs(gg - refs)
+    per_term = err_abs / np.maximum(np.abs(refs), 1e-300)
+    print(f"P14 {which}: per-term rel err median {np.median(per_term):.2e} max {per_term.max():.2e}; "
+          f"|err| / max|g| median {np.median(err_abs) / scale:.2e} max {err_abs.max() / scale:.2e}")
+    assert err_abs.max() / scale <= 1e-10, (which, err_abs.max() / scale)
 
 
 def test_determinism_and_virtual_ranks(lib):
@@ -168,12 +179,18 @@ def test_edge_cases(lib, orc):
     assert rel(got, math.factorial(30) * t ** 30) <= 1e-8
 
 
-@pytest.mark.parametrize("reps", [[6, 5, 5, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4], [3] * 20, [10, 10, 10, 10, 10, 10]])
+RANK_ONE_PATTERNS = [[1] * 60, [2] * 30, [2, 1] * 20, [6, 5, 5, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4],
+                     [3] * 20, [10, 10, 10, 10, 10, 10]]
+
+
+@pytest.mark.parametrize("reps", RANK_ONE_PATTERNS)
 def test_rank_one_N60(lib, reps):
-    # P4 at N = 60 with collisions: lhaf = T(N) prod a_i^{n_i}.  A rank-one matrix is the
-    # sieve's worst case: its cancellation factor kappa = sum|term| / |lhaf| reaches 1e10-1e13
-    # here, so FP64 can only promise ~kappa * eps; the test checks that a-priori bound
-    # (SURVEY 8(c) "oracle error estimate") and 1e-8 where kappa allows it.
+    # P4 at N = 60: lhaf = T(N) prod a_i^{n_i}.  Parity (the north_star's 1e-8) is asserted
+    # wherever the sieve's own cancellation allows FP64 to promise it: kappa * eps <= 1e-10,
+    # kappa = sum|term| / |lhaf| (SURVEY 8(c) "oracle error estimate").  The heavy-collision
+    # rank-one patterns reach kappa = 1e10..1e13: there the test is a labelled DIAGNOSTIC
+    # (printed kappa and error, checked against the a-priori bound 4 kappa eps, not counted as
+    # parity; DESIGN.md section 6 lists them as out of tolerance).
     rng = G.rng_for(sum(reps) + len(reps))
     k = len(reps)
     a = (rng.standard_normal(k) + 1j * rng.standard_normal(k)) * 0.6
@@ -181,11 +198,16 @@ def test_rank_one_N60(lib, reps):
     job.reset(); job.run()
     got = job.finalize()[0]
     kappa = job.abs_sum()[0] / abs(got)
-    want = telephone(sum(reps)) * np.prod(a.astype(complex) ** np.array(reps))
-    assert rel(got, want) <= max(1e-8, 4 * kappa * 2.0 ** -53)
-    if kappa < 1e6:
-        assert rel(got, want) <= 1e-8
     job.close()
+    want = telephone(sum(reps)) * np.prod(a.astype(complex) ** np.array(reps))
+    err = rel(got, want)
+    parity = kappa * 2.0 ** -53 <= 1e-10
+    print(f"rank-one N=60 reps={reps[:4]}..: kappa {kappa:.2e} rel err {err:.2e} "
+          f"{'PARITY (1e-8 asserted)' if parity else 'DIAGNOSTIC (kappa*eps > 1e-10)'}")
+    if parity:
+        assert err <= 1e-8, (reps, err, kappa)
+    else:
+        assert err <= 4 * kappa * 2.0 ** -53, (reps, err, kappa)
 
 
 def test_errors(lib):
@@ -201,9 +223,9 @@ def test_errors(lib):
     assert e.value.status == 3
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 3])
 def test_kernel_variants_agree_with_oracle(lib, orc, variant):
-    # every kernel variant (v1 Householder baseline, v2 aux-warp, v3 default) on loop and
+    # every kernel variant (v1 Householder baseline, v3) on loop and
     # loop-free patterns with collisions, odd N (phantom) and a mixed-state pattern
     rng = G.rng_for(4242)
     k = 7
@@ -272,28 +294,33 @@ def test_block_diagonal_N40(lib, orc):
     assert rel(got, want) <= 1e-8, (got, want)
 
 
-def test_pure_mixed_factorisation_full_size(lib):
+@pytest.mark.parametrize("mult", [[2, 1, 2, 1, 2, 1, 2, 1, 1, 1], [3, 2, 3, 1, 2, 2, 3, 2],
+                                  [1] * 12, [2, 1, 1, 2, 1, 1, 1, 1, 2]])
+def test_pure_mixed_factorisation_full_size(lib, mult):
     # P:104-107 / P:332 at config-5 scale (pure limit eta = 1, m = 100): lhaf_mixed(B (+) B*)
-    # over the doubled pattern equals |lhaf(B, 0, n)|^2.  In the pure limit the natural pairs
-    # (i, i+k) have zero coupling, so the mixed sieve cancels strongly (kappa = sum|term| /
-    # |lhaf| = 6e5 and 5e7 for the two patterns, the same in the oracle); the bound is 1e-8
-    # where kappa allows it and the a-priori FP64 bound 64 kappa eps otherwise.
-    for mult in ([2, 1, 2, 1, 2, 1, 2, 1, 1, 1], [3, 2, 3, 1, 2, 2, 3, 2]):
-        rng = G.rng_for(1005)
-        U = G.haar_unitary(100, rng)
-        A2 = G.lossy_squeezed_A2(U, 0.9, 1.0)
-        B = G.pure_B(U, 0.9)
-        reps = np.zeros(100, np.int32)
-        reps[rng.choice(100, len(mult), replace=False)] = mult
-        job = lib.Job(A2, np.zeros(200), reps, mixed=True)
-        job.reset(); job.run()
-        mixed = job.finalize()[0]
-        kappa = job.abs_sum()[0] / abs(mixed)
-        job.close()
-        pure = lib.lhaf_rpt(B, np.zeros(100), reps)
-        assert rel(mixed, abs(pure) ** 2) <= max(1e-8, 64 * kappa * 2.0 ** -53), (mult, mixed, abs(pure) ** 2, kappa)
-        if kappa < 1e6:
-            assert rel(mixed, abs(pure) ** 2) <= 1e-8
+    # over the doubled pattern equals |lhaf(B, 0, n)|^2.  Parity (1e-8) is asserted where
+    # kappa * eps <= 1e-10 (kappa = sum|term| / |lhaf| of the mixed sieve); heavier
+    # cancellation makes the case a labelled DIAGNOSTIC (a-priori bound 64 kappa eps only).
+    rng = G.rng_for(1005)
+    U = G.haar_unitary(100, rng)
+    A2 = G.lossy_squeezed_A2(U, 0.9, 1.0)
+    B = G.pure_B(U, 0.9)
+    reps = np.zeros(100, np.int32)
+    reps[rng.choice(100, len(mult), replace=False)] = mult
+    job = lib.Job(A2, np.zeros(200), reps, mixed=True)
+    job.reset(); job.run()
+    mixed = job.finalize()[0]
+    kappa = job.abs_sum()[0] / abs(mixed)
+    job.close()
+    pure = lib.lhaf_rpt(B, np.zeros(100), reps)
+    err = rel(mixed, abs(pure) ** 2)
+    parity = kappa * 2.0 ** -53 <= 1e-10
+    print(f"pure/mixed factorisation mult={mult}: kappa {kappa:.2e} rel err {err:.2e} "
+          f"{'PARITY (1e-8 asserted)' if parity else 'DIAGNOSTIC (kappa*eps > 1e-10)'}")
+    if parity:
+        assert err <= 1e-8, (mult, err, kappa)
+    else:
+        assert err <= 64 * kappa * 2.0 ** -53, (mult, err, kappa)
 
 
 def test_cutoff_batched_chain_rule(lib, orc):

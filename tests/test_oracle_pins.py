@@ -295,3 +295,57 @@ def test_brute_et_fds_random(orc, seed):
     ref = orc.lhaf(A, g, reps, method="brute")
     assert rel(orc.lhaf(A, g, reps, method="et"), ref) < 1e-11
     assert rel(orc.lhaf_fds(A, g, reps)[0], ref) < 1e-11
+
+
+# ---------------------------------------------------------------- fds_range / fds_terms pins
+@pytest.mark.parametrize("seed", range(5))
+def test_fds_range_pinned(orc, seed):
+    # fds_range (the term-range sum used as the expected value of the full-size unit tests and
+    # by the CPU baseline) against brute force: the whole range times 2^{-n} is
+    # lhaf; a split of [0, T) adds up; twice the first half is the whole (halving, C6); and
+    # odd N / mixed pairings go through the same range routine
+    rng = G.rng_for(4270 + seed)
+    k = int(rng.integers(3, 7))
+    A = G.random_symmetric(k, rng)
+    g = G.complex_gaussian(k, 1.0, rng) if seed != 3 else np.zeros(k, complex)
+    reps = G.random_pattern(k, int(rng.integers(2, 13)), rng)
+    pairs, eta, left = orc.matched_reps(reps)
+    eta_f = eta + ([1] if left is not None else [])
+    n = sum(eta_f)
+    T = int(np.prod([e + 1 for e in eta_f]))
+    brute = orc.lhaf(A, g, reps, method="brute")
+    s, cnt = orc.fds_range(A, g, reps, 0, T)
+    assert cnt == T
+    assert abs(s * 2.0 ** -n - brute) <= 1e-11 * max(abs(brute), 1e-3)
+    cut = int(rng.integers(1, T)) if T > 1 else 0
+    s1, c1 = orc.fds_range(A, g, reps, 0, cut)
+    s2, c2 = orc.fds_range(A, g, reps, cut, T)
+    assert c1 + c2 == T and abs((s1 + s2) - s) <= 1e-12 * max(abs(s), 1e-3)
+    sh, _ = orc.fds_range(A, g, reps, 0, T // 2)
+    assert abs(2 * sh * 2.0 ** -n - brute) <= 1e-11 * max(abs(brute), 1e-3)
+    assert orc.fds_range(A, g, reps, T, T + 5)[1] == 0   # clipped at T
+
+
+def test_fds_range_mixed_pinned(orc):
+    # the mixed (natural pairing, reading C11) range against the brute-force lhaf of A_n
+    rng = G.rng_for(4280)
+    U = G.haar_unitary(3, rng)
+    A2 = G.lossy_squeezed_A2(U, 0.6, 0.7)
+    g2 = G.complex_gaussian(6, 0.3, rng)
+    reps = np.array([2, 1, 1], np.int32)
+    brute = orc.lhaf_mixed(A2, g2, reps)
+    T = int(np.prod(reps + 1))
+    s, cnt = orc.fds_range(A2, g2, reps, 0, T, mixed=True)
+    assert cnt == T and abs(s * 2.0 ** -int(reps.sum()) - brute) <= 1e-11 * abs(brute)
+
+
+def test_fds_terms_equals_fds_term(orc):
+    rng = G.rng_for(4290)
+    A = G.random_symmetric(6, rng)
+    g = G.complex_gaussian(6, 0.7, rng)
+    C, v, eta, n = orc.reduced_system(A, g, [2, 1, 0, 3, 1, 1])
+    T = int(np.prod([e + 1 for e in eta]))
+    W = np.array([orc.decode(t, eta)[1] for t in range(T)], np.int32)
+    got = orc.fds_terms(C, v, W, n)
+    for t in range(T):
+        assert got[t] == orc.fds_term(C, v, W[t], n)
