@@ -266,9 +266,9 @@ lhaf_status lhaf_rank_info(int32_t *rank, int32_t *nranks);
 lhaf_status lhaf_shard_units(uint64_t units, int32_t rank, int32_t nranks, uint64_t *begin,
                              uint64_t *end);
 
-/* Kernel override for experiments and cross-checks: 0 = automatic (v5 for E > 32, v3 below),
- * 1 = the Householder baseline (lhaf_kernels.cu), 3 = v3 for every size, 5 = v5 where it
- * applies.  Errors: E_ARG for any other id. */
+/* Kernel override for experiments and cross-checks: 0 = automatic (v3), 1 = the Householder
+ * baseline (lhaf_kernels.cu), 3 = v3, 5 = v5 for bordered sizes 33 <= E <= 64 (v3 below) --
+ * three independent reduction codes.  Errors: E_ARG for any other id. */
 lhaf_status lhaf_set_kernel(int32_t variant);
 
 const char *lhaf_last_error(void);

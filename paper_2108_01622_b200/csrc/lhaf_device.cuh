@@ -64,6 +64,9 @@ __device__ __forceinline__ double2 crecip(double2 a) {
 __device__ __forceinline__ double2 shfl2(double2 v, int src) {
   return make_double2(__shfl_sync(LHAF_FULL, v.x, src), __shfl_sync(LHAF_FULL, v.y, src));
 }
+__device__ __forceinline__ double2 shfl2_down(double2 v, int d) {
+  return make_double2(__shfl_down_sync(LHAF_FULL, v.x, d), __shfl_down_sync(LHAF_FULL, v.y, d));
+}
 __device__ __forceinline__ double2 shfl2_xor(double2 v, int m) {
   return make_double2(__shfl_xor_sync(LHAF_FULL, v.x, m), __shfl_xor_sync(LHAF_FULL, v.y, m));
 }

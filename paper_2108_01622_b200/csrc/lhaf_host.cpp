@@ -454,6 +454,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       e = cudaMemcpy(j->d_gamma, gamma, gamma_len * sizeof(double2), cudaMemcpyHostToDevice);
   }
   j->variant = g_ctx.variant ? g_ctx.variant : choose_variant(j->e_max, j->n_max);
+  if (j->variant == 0 || (j->variant == 5 && !v5_supported(j->e_max))) j->variant = 3;
   if (j->variant >= 3 && !bordered_supported(j->e_max, j->n_max)) j->variant = 1;
   if (e == cudaSuccess) e = (j->variant >= 3) ? launch_prep_bordered(j->dev(), 0) : launch_prep(j->dev(), j->d_max, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -466,6 +467,8 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
 }
 
 static cudaError_t run_sieve(lhaf_job *j, uint64_t b, uint64_t e, cudaStream_t st) {
+  if (j->variant == 5)
+    return launch_sieve_v5(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st);
   if (j->variant == 3)
     return launch_sieve_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st);
   return launch_sieve(j->dev(), j->variant, j->d_max, j->n_max, b, e, g_ctx.num_sms, st);
@@ -561,8 +564,8 @@ lhaf_status lhaf_set_device(int32_t device) {
 }
 
 lhaf_status lhaf_set_kernel(int32_t variant) {
-  if (variant < 0 || variant > 3 || variant == 2)
-    return fail(LHAF_E_ARG, "unknown kernel variant %d (0 = default, 1 = Householder, 3 = v3)", variant);
+  if (variant != 0 && variant != 1 && variant != 3 && variant != 5)
+    return fail(LHAF_E_ARG, "unknown kernel variant %d (0 = default, 1 = Householder, 3 = v3, 5 = v5)", variant);
   g_ctx.variant = variant;
   return LHAF_OK;
 }
@@ -583,7 +586,7 @@ lhaf_status lhaf_job_info_get(const lhaf_job *j, lhaf_job_info *info) {
   for (const auto &D : j->descs)
     if (D.d > 0) {
       const bool lp = (D.flags & FLAG_LOOP) != 0;
-      info->flops_per_term_model = (j->variant == 3)   ? v3_flops_per_term(D.d, D.n, lp)
+      info->flops_per_term_model = (j->variant >= 3)   ? v3_flops_per_term(D.d, D.n, lp)
                                                        : flops_per_term(j->variant, D.d, D.n, true);
       break;
     }
@@ -675,7 +678,8 @@ lhaf_status lhaf_job_terms(lhaf_job *j, const uint64_t *t, int32_t nt, double *g
   cudaError_t e = cudaMemcpy(dt, t, nt * sizeof(uint64_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
     const PatDesc &D0 = j->descs[0];
-    e = (j->variant == 3)   ? launch_terms_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
+    e = (j->variant == 5)   ? launch_terms_v5(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
+        : (j->variant == 3) ? launch_terms_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
                             : launch_terms(j->dev(), j->variant, D0.d, D0.n, dt, nt, dg, 0);
   }
   if (e == cudaSuccess) e = cudaMemcpy(g_out, dg, nt * sizeof(double2), cudaMemcpyDeviceToHost);
@@ -758,7 +762,7 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
   if (shared) s = job_create_impl(A, gamma, 0, nullptr, k, (int)groups.size(), 0, false, &j, &groups);
   // the shared groups carry the batched self-pair (and a phantom for odd counts), so they can
   // exceed the kernels' d limit where every per-count pattern still fits: fall back then too
-  if (!shared || (s == LHAF_OK && j->variant != 3) || s == LHAF_E_TOO_LARGE) {
+  if (!shared || (s == LHAF_OK && j->variant == 1) || s == LHAF_E_TOO_LARGE) {
     if (j) { job_free(j); j = nullptr; }
     std::vector<int32_t> reps((size_t)(n_cut + 1) * k);  // separate sieve per count
     for (int c = 0; c <= n_cut; ++c) {

@@ -501,6 +501,9 @@ double flops_per_term(int variant, int d, int n, bool loops) {
 }
 
 int bordered_supported(int e_max, int n_max) { return e_max <= 64 && n_max + 2 <= 255; }
+// automatic choice: v3 (measured fastest at every size); v1 beyond its
+// limits.  v5 (a second data layout) is selected explicitly (lhaf_set_kernel(5)) and by the
+// precise mode.
 int choose_variant(int e_max, int n_max) { return bordered_supported(e_max, n_max) ? 3 : 1; }
 
 }  // namespace lhaf

@@ -33,12 +33,11 @@
 #include <cstdlib>
 #include <cstdio>
 #include "lhaf_device.cuh"
+#include "lhaf_tail.cuh"
 
 namespace lhaf {
 namespace v3 {
-
-__constant__ double c_inv[256];  // 1/m for the series recursions
-static bool g_inv_ready = false;
+using namespace tail;
 
 // Phase timing (diagnostic builds only, -DLHAF_PHASE_TIMING): cycles of thread 0 of every
 // team spent in decode/build, reduction, band -> F, La Budde, hand-off, end barrier.
@@ -124,17 +123,6 @@ __device__ __forceinline__ int opaque(int x) {
   return x;
 }
 
-template <int NW, int TEAMS>
-__device__ __forceinline__ void team_sync(int team) {
-  if constexpr (NW == 1) {
-    __syncwarp();
-  } else if constexpr (TEAMS == 1) {
-    __syncthreads();
-  } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(32 * NW) : "memory");
-  }
-}
-
 // Shared memory of one team (double2 words), for a pattern with (E, NTL, n):
 //   hb   [E][NTL]       band of H (unit subdiagonal): [j][1] = H[j][j], [j][1+m] = H[j][j+m]
 //   u1   union { cand [2][NW][CC] | kb [2][RC] | keys [2][NW] | piv [2][NW] } (reduction)
@@ -190,318 +178,6 @@ __device__ __forceinline__ Pattern pattern_of(const PatDesc &P) {
   D.E = opaque(P.d) + D.o;
   D.NTL = min(D.n + 1 + D.o, D.E + 1);
   return D;
-}
-
-// ---------------------------------------------------------------- La Budde (one warp)
-// Trailing La Budde on the top NTL coefficients (t = distance from the leading coefficient):
-//   q_j[t] = q_{j+1}[t] - h_jj q_{j+1}[t-1] + S_j[t],
-//   S_j[t] = - sum_{m=1}^{min(t-1, E-1-j)} F_j[m] q_{j+m+1}[t-m-1]     (F_j[m] = hb[j][1+m]).
-// S_j needs only rows j+2.. (already final), so iteration j computes S_{j-1} ahead of the
-// short loop-carried chain q_{j+1} -> q_j (a shuffle and two FMAs).  Lane t holds q_{j+1}[t]
-// in registers (NRT registers per lane: NTL <= 32 NRT); rows go to Q[j][t] for the m-sums.
-template <int NRT>
-__device__ __forceinline__ void labudde(const double2 *hb, double2 *Q, int E, int NTL, int lane) {
-  double2 qn[NRT], S[NRT];
-#pragma unroll
-  for (int r = 0; r < NRT; ++r) {
-    const int t = lane + 32 * r;
-    qn[r] = (t == 0) ? c1() : c0();  // q_E = 1
-    S[r] = c0();                     // S_{E-1} = 0
-    if (t < NTL) Q[E * NTL + t] = qn[r];
-  }
-  __syncwarp();
-  for (int j = E - 1; j >= 0; --j) {
-    // S_{j-1}[t] from rows j+1 .. E (final); groups of 4 terms under a warp-uniform bound
-    double2 Sn[NRT];
-#pragma unroll
-    for (int r = 0; r < NRT; ++r) {
-      const int t = lane + 32 * r;
-      double2 a0 = c0(), a1 = c0(), a2 = c0(), a3 = c0();
-      const int mm = (j >= 1 && t < NTL && t <= E - j + 1) ? min(t - 1, E - j) : 0;
-      const int mw = min(min(NTL, 32 * (r + 1)) - 2, E - j);  // max of mm over the warp
-      if (j >= 1) {
-        const double2 *F = hb + (j - 1) * NTL + 1;  // F_{j-1}[m] = F[m]
-        const double2 *qd = Q + (j + 1) * NTL + t - 2;  // q_{j+m}[t-m-1] at m = 1
-        for (int m = 1; m <= mw; m += 4, qd += 4 * (NTL - 1)) {
-          if (m <= mm) a0 = cfma(F[m], qd[0], a0);
-          if (m + 1 <= mm) a1 = cfma(F[m + 1], qd[NTL - 1], a1);
-          if (m + 2 <= mm) a2 = cfma(F[m + 2], qd[2 * (NTL - 1)], a2);
-          if (m + 3 <= mm) a3 = cfma(F[m + 3], qd[3 * (NTL - 1)], a3);
-        }
-      }
-      Sn[r] = make_double2(-((a0.x + a1.x) + (a2.x + a3.x)), -((a0.y + a1.y) + (a2.y + a3.y)));
-    }
-    // q_j from q_{j+1} (registers) and S_j
-    const double2 h = hb[j * NTL + 1];
-    double2 shfl_last[NRT];  // q_{j+1}[32 r + 31], for lane 0 of register r + 1
-#pragma unroll
-    for (int r = 0; r < NRT; ++r) shfl_last[r] = shfl2(qn[r], 31);
-    double2 up[NRT];  // q_{j+1}[t-1]
-#pragma unroll
-    for (int r = 0; r < NRT; ++r) {
-      const double2 s = shfl2(qn[r], (lane + 31) & 31);  // all lanes shuffle (full mask)
-      up[r] = (lane != 0) ? s : (r == 0 ? c0() : shfl_last[r - 1]);
-    }
-#pragma unroll
-    for (int r = 0; r < NRT; ++r) {
-      const int t = lane + 32 * r;
-      double2 q = cadd(S[r], cfms(h, up[r], qn[r]));
-      if (t > E - j) q = c0();  // above the degree of q_j
-      qn[r] = q;
-      if (t < NTL) Q[j * NTL + t] = q;
-      S[r] = Sn[r];
-    }
-    __syncwarp();
-  }
-}
-
-// Team version: warp w sums the m = 1 + w (mod NW) part of S_{j-1} into part[j&1][w][t];
-// warp 0 keeps q_{j+1} in registers and forms q_j = q_{j+1} - h q_{j+1}[t-1] - sum_w part;
-// one team barrier per row.
-template <int NRT, int NW, int TEAMS>
-__device__ __forceinline__ void labudde_team(const double2 *hb, double2 *Q, double2 *part, int E,
-                                             int NTL, int warp, int lane, int team) {
-  double2 qn[NRT];
-#pragma unroll
-  for (int r = 0; r < NRT; ++r) {
-    const int t = lane + 32 * r;
-    qn[r] = (t == 0) ? c1() : c0();  // q_E = 1
-    if (warp == 0 && t < NTL) Q[E * NTL + t] = qn[r];
-  }
-  team_sync<NW, TEAMS>(team);
-  for (int j = E - 1; j >= 0; --j) {
-    // partial m-sums of S_{j-1} (rows j+1 .. E are final)
-    double2 *pw = part + ((j & 1) * NW + warp) * NTL;
-#pragma unroll
-    for (int r = 0; r < NRT; ++r) {
-      const int t = lane + 32 * r;
-      double2 a0 = c0(), a1 = c0(), a2 = c0(), a3 = c0();
-      const int mm = (j >= 1 && t < NTL && t <= E - j + 1) ? min(t - 1, E - j) : 0;
-      const int mw = min(min(NTL, 32 * (r + 1)) - 2, E - j);  // max of mm over the warp
-      if (j >= 1) {
-        const double2 *F = hb + (j - 1) * NTL + 1;  // F_{j-1}[m] = F[m]
-        int m = 1 + warp;
-        const double2 *qd = Q + (j + m) * NTL + t - m - 1;  // q_{j+m}[t-m-1]
-        for (; m <= mw; m += 4 * NW, qd += 4 * NW * (NTL - 1)) {  // warp-uniform bound
-          if (m <= mm) a0 = cfma(F[m], qd[0], a0);
-          if (m + NW <= mm) a1 = cfma(F[m + NW], qd[NW * (NTL - 1)], a1);
-          if (m + 2 * NW <= mm) a2 = cfma(F[m + 2 * NW], qd[2 * NW * (NTL - 1)], a2);
-          if (m + 3 * NW <= mm) a3 = cfma(F[m + 3 * NW], qd[3 * NW * (NTL - 1)], a3);
-        }
-      }
-      a0 = cadd(a0, a2);
-      a1 = cadd(a1, a3);
-      if (t < NTL) pw[t] = cadd(a0, a1);
-    }
-    if (warp == 0) {
-      // q_j = q_{j+1} - h_jj q_{j+1}[t-1] - S_j, S_j = sum of the partials written at j+1
-      const double2 h = hb[j * NTL + 1];
-      const double2 *pp = part + ((j + 1) & 1) * NW * NTL;
-      double2 last[NRT], up[NRT];
-#pragma unroll
-      for (int r = 0; r < NRT; ++r) last[r] = shfl2(qn[r], 31);
-#pragma unroll
-      for (int r = 0; r < NRT; ++r) {
-        const double2 s = shfl2(qn[r], (lane + 31) & 31);
-        up[r] = (lane != 0) ? s : (r == 0 ? c0() : last[r - 1]);
-      }
-#pragma unroll
-      for (int r = 0; r < NRT; ++r) {
-        const int t = lane + 32 * r;
-        double2 q = cfms(h, up[r], qn[r]);
-        if (j + 1 < E && t < NTL) {
-#pragma unroll
-          for (int w = 0; w < NW; ++w) q = csub(q, pp[w * NTL + t]);
-        }
-        if (t > E - j) q = c0();  // above the degree of q_j
-        qn[r] = q;
-        if (t < NTL) Q[j * NTL + t] = q;
-      }
-    }
-    team_sync<NW, TEAMS>(team);
-  }
-}
-
-// out[t] = q[t - d] (0 for t < d) over the NRT registers of a warp; d warp-uniform in [1, 31]
-template <int NRT>
-__device__ __forceinline__ void shift_up(const double2 (&q)[NRT], int d, int lane,
-                                         double2 (&out)[NRT]) {
-  double2 sh[NRT];
-#pragma unroll
-  for (int r = 0; r < NRT; ++r) sh[r] = shfl2(q[r], (lane - d) & 31);
-#pragma unroll
-  for (int r = 0; r < NRT; ++r) out[r] = (lane >= d) ? sh[r] : (r == 0 ? c0() : sh[r - 1]);
-}
-
-// Team version, two rows per barrier.  Block b forms rows j = E-1-2b and j-1 in warp 0:
-//   q_j     = q_{j+1} - h_j q_{j+1}[t-1]     - P_j     - F_j[1] q_{j+2}[t-2]
-//   q_{j-1} = q_j     - h_{j-1} q_j[t-1]     - P_{j-1} - F_{j-1}[1] q_{j+1}[t-2]
-//                                                      - F_{j-1}[2] q_{j+2}[t-3]
-// with q_{j+1}, q_{j+2} (the previous block's rows) held in registers, while every warp sums,
-// for the next block's rows r = j-2, j-3, the m-terms on rows >= j+1 (m >= j - r), split
-// m = m0 + w (mod NW): P_r[t] = sum_m F_r[m] q_{r+m+1}[t-m-1] into part[b&1][w][r][t].
-template <int NRT, int NW, int TEAMS>
-__device__ __forceinline__ void labudde_team2(const double2 *hb, double2 *Q, double2 *part, int E,
-                                              int NTL, int warp, int lane, int team) {
-  double2 qa[NRT], qb[NRT];  // q_{j+1}, q_{j+2}
-#pragma unroll
-  for (int r = 0; r < NRT; ++r) {
-    const int t = lane + 32 * r;
-    qa[r] = (t == 0) ? c1() : c0();  // q_E = 1
-    qb[r] = c0();                    // (q_{E+1}: no such row)
-    if (warp == 0 && t < NTL) Q[E * NTL + t] = qa[r];
-    if (t < NTL) {  // the partials of block 0 (none)
-      part[(NW + warp) * 2 * NTL + t] = c0();
-      part[(NW + warp) * 2 * NTL + NTL + t] = c0();
-    }
-  }
-  team_sync<NW, TEAMS>(team);
-  for (int b = 0, j = E - 1; j >= 0; ++b, j -= 2) {
-    // partial m-sums for rows j-2 (slot 0) and j-3 (slot 1) from rows >= j+1 (final)
-    double2 *pw = part + ((b & 1) * NW + warp) * 2 * NTL;
-#pragma unroll
-    for (int sl = 0; sl < 2; ++sl) {
-      const int rw = j - 2 - sl, m0 = 2 + sl;
-#pragma unroll
-      for (int r = 0; r < NRT; ++r) {
-        const int t = lane + 32 * r;
-        double2 a0 = c0(), a1 = c0(), a2 = c0(), a3 = c0();
-        if (rw >= 0) {
-          const int mm = (t < NTL && t <= E - rw) ? min(t - 1, E - 1 - rw) : 0;
-          const int mw = min(min(NTL, 32 * (r + 1)) - 2, E - 1 - rw);  // max of mm over the warp
-          const double2 *F = hb + rw * NTL + 1;                        // F_r[m] = F[m]
-          int m = m0 + warp;
-          const double2 *qd = Q + (rw + m + 1) * NTL + t - m - 1;       // q_{r+m+1}[t-m-1]
-          for (; m <= mw; m += 4 * NW, qd += 4 * NW * (NTL - 1)) {     // warp-uniform bound
-            if (m <= mm) a0 = cfma(F[m], qd[0], a0);
-            if (m + NW <= mm) a1 = cfma(F[m + NW], qd[NW * (NTL - 1)], a1);
-            if (m + 2 * NW <= mm) a2 = cfma(F[m + 2 * NW], qd[2 * NW * (NTL - 1)], a2);
-            if (m + 3 * NW <= mm) a3 = cfma(F[m + 3 * NW], qd[3 * NW * (NTL - 1)], a3);
-          }
-        }
-        if (t < NTL) pw[sl * NTL + t] = cadd(cadd(a0, a2), cadd(a1, a3));
-      }
-    }
-    if (warp == 0) {
-      const double2 *pp = part + (((b + 1) & 1) * NW) * 2 * NTL;  // written in block b-1
-      double2 u1[NRT], u2[NRT], u3[NRT];
-      // row j
-      {
-        const double2 h = hb[j * NTL + 1];
-        const double2 f1 = (E - 1 - j >= 1 && NTL > 2) ? hb[j * NTL + 2] : c0();
-        shift_up<NRT>(qa, 1, lane, u1);
-        shift_up<NRT>(qb, 2, lane, u2);
-#pragma unroll
-        for (int r = 0; r < NRT; ++r) {
-          const int t = lane + 32 * r;
-          double2 q = cfms(h, u1[r], qa[r]);
-          q = cfms(f1, u2[r], q);
-          if (t < NTL) {
-#pragma unroll
-            for (int w = 0; w < NW; ++w) q = csub(q, pp[w * 2 * NTL + t]);
-          }
-          if (t > E - j) q = c0();  // above the degree of q_j
-          qb[r] = q;                // (qb <- q_j, qa stays q_{j+1} for row j-1)
-          if (t < NTL) Q[j * NTL + t] = q;
-        }
-      }
-      // row j-1: q_{j+1} = qa, q_j = qb, q_{j+2} = u2 shifted by 2 (recompute by 3)
-      if (j >= 1) {
-        const int i = j - 1;
-        const double2 h = hb[i * NTL + 1];
-        const double2 f1 = (NTL > 2) ? hb[i * NTL + 2] : c0();  // (E-1-i >= 1)
-        const double2 f2 = (E - 1 - i >= 2 && NTL > 3) ? hb[i * NTL + 3] : c0();
-        double2 s1[NRT];
-        shift_up<NRT>(qb, 1, lane, s1);  // q_j[t-1]
-        shift_up<NRT>(qa, 2, lane, u1);  // q_{j+1}[t-2]
-        // q_{j+2}[t-3] = u2 (q_{j+2}[t-2]) shifted by one more
-        shift_up<NRT>(u2, 1, lane, u3);
-#pragma unroll
-        for (int r = 0; r < NRT; ++r) {
-          const int t = lane + 32 * r;
-          double2 q = cfms(h, s1[r], qb[r]);
-          q = cfms(f1, u1[r], q);
-          q = cfms(f2, u3[r], q);
-          if (t < NTL) {
-#pragma unroll
-            for (int w = 0; w < NW; ++w) q = csub(q, pp[w * 2 * NTL + NTL + t]);
-          }
-          if (t > E - i) q = c0();
-          qa[r] = q;  // q_{j-1}: the next block's q_{j'+1}; qb = q_j its q_{j'+2}
-          if (t < NTL) Q[i * NTL + t] = q;
-        }
-      }
-    }
-    team_sync<NW, TEAMS>(team);
-  }
-}
-
-// ---------------------------------------------------------------- series (one warp)
-// g = [lam^n] c_M^{-1/2} exp(S/2), lam S = 1 - c_B / c_M (loops), by column sweeps: lane m
-// holds the accumulators of coefficients m, m+32, ... (NR registers, n + 2 <= 32 NR):
-//   m Q_m = -sum_{i=1}^{m} (m - i/2) c_i Q_{m-i}   (c = c_M),  R = (c_M - c_B) / c_M,
-//   m E_m = 1/2 sum_{j=1}^{m} j S_j E_{m-j},  S_j = R_{j+1},  g = sum_m Q_m E_{n-m}.
-// Finished coefficients go to scratch (Qs, Rs, Es: 3 (n+2) words).
-template <int NR>
-__device__ __forceinline__ double2 series(const double2 *cM, const double2 *cB, int n, int NTL,
-                                          bool loops, double2 *scratch, int lane) {
-  double2 *Qs = scratch, *Rs = Qs + (n + 2), *Es = Rs + (n + 2);
-  double2 qa[NR], ra[NR];
-  double md[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const int m = lane + 32 * r;
-    md[r] = (double)m;
-    qa[r] = c0();
-    ra[r] = (loops && m <= n + 1 && m < NTL) ? csub(cM[m], cB[m]) : c0();
-  }
-  const int jmax = loops ? n + 1 : n;
-  double jd = 0.0;
-  for (int j = 0; j <= jmax; ++j, jd += 1.0) {
-    const int lj = j & 31, rj = j >> 5;
-    double2 qs = qa[0], rs = ra[0];
-#pragma unroll
-    for (int r = 1; r < NR; ++r)
-      if (rj == r) { qs = qa[r]; rs = ra[r]; }
-    double2 qj = (j == 0) ? c1() : cscale(qs, -c_inv[j]);
-    qj = shfl2(qj, lj);
-    const double2 rv = shfl2(rs, lj);
-    if (lane == lj) { Qs[j] = qj; Rs[j] = rv; }
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const int m = lane + 32 * r;
-      if (m > j && m <= jmax && m - j < NTL) {
-        const double2 c = cM[m - j];
-        if (m <= n) qa[r] = cfma(cscale(c, 0.5 * (md[r] + jd)), qj, qa[r]);
-        if (loops) ra[r] = cfms(c, rv, ra[r]);
-      }
-    }
-  }
-  __syncwarp();
-  if (!loops) return Qs[n];
-  double2 ea[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) ea[r] = c0();
-  double id = 0.0;
-  for (int i = 0; i <= n; ++i, id += 1.0) {
-    const int li = i & 31, ri = i >> 5;
-    double2 es = ea[0];
-#pragma unroll
-    for (int r = 1; r < NR; ++r)
-      if (ri == r) es = ea[r];
-    double2 ei = (i == 0) ? c1() : cscale(es, c_inv[i]);
-    ei = shfl2(ei, li);
-    if (lane == li) Es[i] = ei;
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const int m = lane + 32 * r;
-      if (m > i && m <= n) ea[r] = cfma(cscale(Rs[m - i + 1], 0.5 * (md[r] - id)), ei, ea[r]);
-    }
-  }
-  __syncwarp();
-  double2 gp = c0();
-  for (int m = lane; m <= n; m += 32) gp = cfma(Qs[m], Es[n - m], gp);
-  return warp_sum2(gp);
 }
 
 // ================================================================ phased reduction
@@ -1179,15 +855,6 @@ static int alt_mode() {
   return m;
 }
 
-static cudaError_t ensure_inv() {
-  if (g_inv_ready) return cudaSuccess;
-  double h[256];
-  h[0] = 0.0;
-  for (int i = 1; i < 256; ++i) h[i] = 1.0 / (double)i;
-  cudaError_t e = cudaMemcpyToSymbol(c_inv, h, sizeof h);
-  if (e == cudaSuccess) g_inv_ready = true;
-  return e;
-}
 
 }  // namespace v3
 

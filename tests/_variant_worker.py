@@ -10,6 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import paper_2108_01622_b200 as L  # noqa: E402
 import _variant_cases as VC  # noqa: E402
 
+if os.environ.get("LHAF_KERNEL"):
+    L.lhaf_set_kernel(int(os.environ["LHAF_KERNEL"]))
 res = []
 for c in VC.cases():
     v = L.lhaf_rpt(c["A"], c["gamma"], c["reps"])

@@ -223,9 +223,9 @@ def test_errors(lib):
     assert e.value.status == 3
 
 
-@pytest.mark.parametrize("variant", [1, 3])
+@pytest.mark.parametrize("variant", [1, 3, 5])
 def test_kernel_variants_agree_with_oracle(lib, orc, variant):
-    # every kernel variant (v1 Householder baseline, v3) on loop and
+    # every kernel variant (v1 Householder baseline, v3, v5) on loop and
     # loop-free patterns with collisions, odd N (phantom) and a mixed-state pattern
     rng = G.rng_for(4242)
     k = 7

@@ -1,6 +1,7 @@
 """Alternative kernel instantiations against the oracle, each in its own process (the choice
 is read once per process from LHAF_V3_ALT): 0 = default (phased reduction), 3 = single-phase
-reduction (a second rounding order of the same method).  Block-diagonal
+reduction (a second rounding order of the same method), and the v5 kernel (LHAF_KERNEL=5: a
+different data layout of the reduction, the third independent code).  Block-diagonal
 matrices with the pairs straddling the blocks: lhaf(A1 (+) A2) = lhaf(A1) lhaf(A2),
 each factor by the oracle's ET tier."""
 import json
@@ -27,9 +28,9 @@ def refs(orc):
     return out
 
 
-@pytest.mark.parametrize("alt", [0, 3])
+@pytest.mark.parametrize("alt", [0, 3, "v5"])
 def test_variant_block_diagonal(lib, refs, alt):
-    env = dict(os.environ, LHAF_V3_ALT=str(alt))
+    env = dict(os.environ, LHAF_V3_ALT=str(alt)) if alt != "v5" else dict(os.environ, LHAF_KERNEL="5")
     r = subprocess.run([sys.executable, os.path.join(HERE, "_variant_worker.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
