@@ -213,6 +213,8 @@ typedef struct {
   uint64_t terms;        /* total evaluated terms (sum of T_eval) */
   double flops_per_term_model; /* algorithmic FP64 flops per term of the selected kernel */
   uint64_t h2d_plan_bytes;     /* bytes of plan tables copied host->device at creation */
+  int32_t precision;           /* precision mode of the job (lhaf_set_precision) */
+  int32_t pad_;
 } lhaf_job_info;
 
 lhaf_status lhaf_job_create(const double *A, const double *gamma, int64_t gamma_stride,
@@ -265,6 +267,18 @@ lhaf_status lhaf_rank_info(int32_t *rank, int32_t *nranks);
  * nranks).  Host-only integer arithmetic. */
 lhaf_status lhaf_shard_units(uint64_t units, int32_t rank, int32_t nranks, uint64_t *begin,
                              uint64_t *end);
+
+/* Precision of the per-term arithmetic ("Precise mode"; the paper's
+ * accuracy discussion P:139-140).  0 (default): every stage in FP64.  1 (precise): the
+ * Hessenberg reduction stays FP64, the characteristic-polynomial recursion (La Budde) and the
+ * power series run in double-double -- the stages that dominate the per-term rounding error --
+ * on the v5 kernel (bordered size E <= 64; larger jobs fail with E_TOO_LARGE); mixed states
+ * are then planned by the natural pairing (i, i+k) (reading C11), whose sieve cancels ~100x
+ * less than the greedy matching of the doubled pattern once its terms are accurate.  Cost: see
+ * DESIGN.md.  Applies to jobs created afterwards.  lhaf_rpt_cutoff keeps FP64.
+ * Errors: E_ARG for another mode. */
+lhaf_status lhaf_set_precision(int32_t mode);
+int32_t lhaf_get_precision(void);
 
 /* Kernel override for experiments and cross-checks: 0 = automatic (v3), 1 = the Householder
  * baseline (lhaf_kernels.cu), 3 = v3, 5 = v5 for bordered sizes 33 <= E <= 64 (v3 below) --

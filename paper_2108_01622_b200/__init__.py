@@ -51,7 +51,8 @@ class PlanInfo(ctypes.Structure):
 class JobInfo(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("d_max", ctypes.c_int32), ("n_max", ctypes.c_int32),
                 ("kernel", ctypes.c_int32), ("units", ctypes.c_uint64), ("terms", ctypes.c_uint64),
-                ("flops_per_term_model", ctypes.c_double), ("h2d_plan_bytes", ctypes.c_uint64)]
+                ("flops_per_term_model", ctypes.c_double), ("h2d_plan_bytes", ctypes.c_uint64),
+                ("precision", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -94,6 +95,7 @@ def _load() -> ctypes.CDLL:
         "lhaf_init_rank": ([ctypes.c_int32, ctypes.c_int32, vp, ctypes.c_int32]),
         "lhaf_rank_info": ([ip, ip]),
         "lhaf_set_kernel": ([ctypes.c_int32]),
+        "lhaf_set_precision": ([ctypes.c_int32]),
         "lhaf_shard_units": ([u64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(u64),
                               ctypes.POINTER(u64)]),
     }
@@ -106,6 +108,7 @@ def _load() -> ctypes.CDLL:
     lib.lhaf_last_error.restype = ctypes.c_char_p
     lib.lhaf_version.restype = ctypes.c_char_p
     lib.lhaf_shutdown.restype = None
+    lib.lhaf_get_precision.restype = ctypes.c_int32
     return lib
 
 
@@ -141,6 +144,7 @@ EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_
             "lhaf_job_finalize", "lhaf_job_abs_sum",
             "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
             "lhaf_get_unique_id", "lhaf_init_rank", "lhaf_rank_info", "lhaf_set_kernel",
+            "lhaf_set_precision", "lhaf_get_precision",
             "lhaf_shard_units", "lhaf_last_error", "lhaf_version", "lhaf_shutdown"]
 
 
@@ -362,6 +366,15 @@ def lhaf_set_device(device: int):
 
 def lhaf_set_kernel(variant: int):
     _check(_lib.lhaf_set_kernel(variant))
+
+
+def lhaf_set_precision(mode: int):
+    """0 = FP64 per term (default), 1 = precise (double-double La Budde + series)."""
+    _check(_lib.lhaf_set_precision(mode))
+
+
+def lhaf_get_precision() -> int:
+    return int(_lib.lhaf_get_precision())
 
 
 def lhaf_get_unique_id() -> bytes:

@@ -83,6 +83,7 @@ struct Ctx {
   int device = -1;
   int num_sms = 0;
   int variant = 0;
+  int precision = 0;  // 0: FP64 per term; 1: precise (double-double La Budde + series, v5)
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   Nccl nccl;
@@ -140,6 +141,8 @@ lhaf_status make_plan(const int32_t *reps, int k, int mixed, Plan &P) {
   if (mixed) N *= 2;
   if (N > 4 * LHAF_MAX_DEGREE) return fail(LHAF_E_TOO_LARGE, "N = %ld photons too large", N);
   P.N = (int)N;
+  // precise mode plans mixed states by the natural pairing (lhaf_set_precision, reading C11)
+  if (mixed == 1 && g_ctx.precision == 1) mixed = 2;
   if (mixed == 1) {
     // mixed state, default: the greedy matching of the doubled pattern (reps, reps) over the
     // 2k modes (the same lhaf as the natural pairing; far better conditioned in FP64 -- the
@@ -248,7 +251,7 @@ int lhaf::set_error(int status, const char *msg) {
 
 // ------------------------------------------------------------------ job
 struct lhaf_job {
-  int batch = 0, kdim = 0, d_max = 0, n_max = 0, variant = 1;
+  int batch = 0, kdim = 0, d_max = 0, n_max = 0, variant = 1, prec = 0;
   int e_max = 0, ntl_max = 0;   // bordered dimension E and leading coefficients NTL
   bool any_loop = false;
   uint64_t units = 0, terms = 0, plan_bytes = 0;
@@ -454,7 +457,13 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       e = cudaMemcpy(j->d_gamma, gamma, gamma_len * sizeof(double2), cudaMemcpyHostToDevice);
   }
   j->variant = g_ctx.variant ? g_ctx.variant : choose_variant(j->e_max, j->n_max);
+  j->prec = g_ctx.precision;
+  if (j->prec) j->variant = 5;  // the precise tail lives in the v5 kernel (every E <= 64)
   if (j->variant == 0 || (j->variant == 5 && !v5_supported(j->e_max))) j->variant = 3;
+  if (j->prec && j->variant != 5) {
+    job_free(j);
+    return fail(LHAF_E_TOO_LARGE, "precise mode needs d <= 63 (bordered size <= 64)");
+  }
   if (j->variant >= 3 && !bordered_supported(j->e_max, j->n_max)) j->variant = 1;
   if (e == cudaSuccess) e = (j->variant >= 3) ? launch_prep_bordered(j->dev(), 0) : launch_prep(j->dev(), j->d_max, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -468,7 +477,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
 
 static cudaError_t run_sieve(lhaf_job *j, uint64_t b, uint64_t e, cudaStream_t st) {
   if (j->variant == 5)
-    return launch_sieve_v5(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st);
+    return launch_sieve_v5(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st, j->prec);
   if (j->variant == 3)
     return launch_sieve_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st);
   return launch_sieve(j->dev(), j->variant, j->d_max, j->n_max, b, e, g_ctx.num_sms, st);
@@ -563,6 +572,14 @@ lhaf_status lhaf_set_device(int32_t device) {
   return ensure_device();
 }
 
+lhaf_status lhaf_set_precision(int32_t mode) {
+  if (mode != 0 && mode != 1) return fail(LHAF_E_ARG, "unknown precision mode %d (0 = FP64, 1 = precise)", mode);
+  g_ctx.precision = mode;
+  return LHAF_OK;
+}
+
+int32_t lhaf_get_precision(void) { return g_ctx.precision; }
+
 lhaf_status lhaf_set_kernel(int32_t variant) {
   if (variant != 0 && variant != 1 && variant != 3 && variant != 5)
     return fail(LHAF_E_ARG, "unknown kernel variant %d (0 = default, 1 = Householder, 3 = v3, 5 = v5)", variant);
@@ -580,6 +597,7 @@ lhaf_status lhaf_job_create(const double *A, const double *gamma, int64_t gamma_
 lhaf_status lhaf_job_info_get(const lhaf_job *j, lhaf_job_info *info) {
   if (!j || !info) return fail(LHAF_E_ARG, "null pointer");
   info->batch = j->batch; info->d_max = j->d_max; info->n_max = j->n_max; info->kernel = j->variant;
+  info->precision = j->prec;
   info->units = j->units; info->terms = j->terms; info->h2d_plan_bytes = j->plan_bytes;
   // model flops of the first non-empty pattern (batches here are uniform in d)
   info->flops_per_term_model = 0.0;
@@ -678,7 +696,7 @@ lhaf_status lhaf_job_terms(lhaf_job *j, const uint64_t *t, int32_t nt, double *g
   cudaError_t e = cudaMemcpy(dt, t, nt * sizeof(uint64_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
     const PatDesc &D0 = j->descs[0];
-    e = (j->variant == 5)   ? launch_terms_v5(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
+    e = (j->variant == 5)   ? launch_terms_v5(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0, j->prec)
         : (j->variant == 3) ? launch_terms_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
                             : launch_terms(j->dev(), j->variant, D0.d, D0.n, dt, nt, dg, 0);
   }

@@ -87,10 +87,11 @@ double v3_flops_per_term(int d, int n, bool loops);
 // Variant 5 (lhaf_v5.cu): 2-D register tile per lane, one barrier per column, 8 warps per team;
 // bordered sizes 33 <= E <= 64.  Same prep (launch_prep_bordered) and flop model as v3.
 int v5_supported(int e_max);
+// prec = 1: the precise tail (double-double La Budde and series, lhaf_dd.cuh)
 cudaError_t launch_sieve_v5(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t unit_begin,
-                            uint64_t unit_end, int num_sms, cudaStream_t s);
+                            uint64_t unit_end, int num_sms, cudaStream_t s, int prec);
 cudaError_t launch_terms_v5(const JobDev &job, int e_max, int ntl_max, int n_max, const uint64_t *t,
-                            int nt, double2 *g_out, cudaStream_t s);
+                            int nt, double2 *g_out, cudaStream_t s, int prec);
 
 // sets lhaf_last_error() for entry points outside lhaf_host.cpp (returns its status argument)
 int set_error(int status, const char *msg);

@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include "lhaf_device.cuh"
 #include "lhaf_tail.cuh"
+#include "lhaf_dd.cuh"
 
 namespace lhaf {
 namespace v5 {
@@ -69,12 +70,14 @@ struct Shape {
   static constexpr int CAND = 0, KB = CAND + 2 * NW * 64, REC = KB + 2 * 64, YV = REC + 2 * NW,
                        CMP = YV + 4 * NW, RED_END = CMP + NW * 4 * 48;
   // band row stride BS = NTL + 1 (odd multiple of 16 B: conflict-free row-strided reads)
-  __host__ __device__ static int u1_words(int E, int NTL, int n) {
-    const int lab = (E + 1) * (NTL + 1) + 3 * (n + 2) + 128 + 2 * NW;  // q rows, series, ring
+  // PREC (double-double tail): q rows, series scratch, level ring and totals twice (hi / lo)
+  __host__ __device__ static int u1_words(int E, int NTL, int n, bool prec) {
+    const int f = prec ? 2 : 1;
+    const int lab = f * ((E + 1) * (NTL + 1) + 3 * (n + 2) + 128 + 2 * NW);
     return RED_END > lab ? RED_END : lab;
   }
-  __host__ __device__ static int words(int E, int NTL, int n) {
-    return (E + 2) * (NTL + 1) + u1_words(E, NTL, n) + 32 + 64 + 1;
+  __host__ __device__ static int words(int E, int NTL, int n, bool prec) {
+    return (E + 2) * (NTL + 1) + u1_words(E, NTL, n, prec) + 32 + 64 + 1;
   }
 };
 
@@ -85,11 +88,11 @@ struct Mem {
   double2 *beta;
 };
 
-template <int NW>
+template <int NW, bool PREC>
 __device__ __forceinline__ Mem carve(double2 *b, int E, int NTL, int n) {
   Mem M;
   M.hb = b; b += (E + 2) * (NTL + 1);
-  M.u1 = b; b += Shape<NW>::u1_words(E, NTL, n);
+  M.u1 = b; b += Shape<NW>::u1_words(E, NTL, n, PREC);
   M.wv = reinterpret_cast<int *>(b); b += 32;
   M.ww = reinterpret_cast<double *>(b); b += 64;
   M.beta = b;
@@ -400,32 +403,45 @@ __device__ unsigned long long g_v5_phase[4];
 #define V5_T2()
 #endif
 
-// a7-a9 of one term in warp 0: level-by-level La Budde on the band (q rows in the reduction's
-// scratch, free by now) and the series; the other warps wait at the end-of-term barrier
-template <int NW>
+// a7-a9 of one term: level-by-level team La Budde on the band (q rows in the reduction's
+// scratch, free by now), then the series in warp 0; PREC: both in double-double (lhaf_dd.cuh)
+template <int NW, bool PREC>
 __device__ __forceinline__ double2 team_tail(const Pattern &D, const Mem &M, int warp, int lane) {
   const int n = D.n, E = D.E, NTL = D.NTL, BS = NTL + 1;
-  double2 *Q = M.u1;
-  double2 *Lr = Q + (E + 1) * BS + 3 * (n + 2);  // [2][64] level ring, then [2][NW] totals
-  if (NTL <= 32) labudde_levels_team<NW, 1, 32>(M.hb, Q, Lr, Lr + 128, E, NTL, BS, warp, lane, 0);
-  else labudde_levels_team<NW, 1, 65>(M.hb, Q, Lr, Lr + 128, E, NTL, BS, warp, lane, 0);
-#ifdef LHAF_V5_TIMING
-  if (threadIdx.x == 0) atomicAdd(&g_v5_phase[3], (unsigned long long)clock64());
-#endif
   double2 g = c0();
-  if (warp == 0) {
-    const double2 *cB = Q;
-    const double2 *cM = D.loops ? Q + BS : Q;
-    double2 *scr = Q + (E + 1) * BS;
-    if (n + 2 <= 32) g = series<1>(cM, cB, n, NTL, D.loops, scr, lane);
-    else if (n + 2 <= 64) g = series<2>(cM, cB, n, NTL, D.loops, scr, lane);
-    else g = series<5>(cM, cB, n, NTL, D.loops, scr, lane);
+  if constexpr (!PREC) {
+    double2 *Q = M.u1;
+    double2 *Lr = Q + (E + 1) * BS + 3 * (n + 2);  // [2][64] level ring, then [2][NW] totals
+    if (NTL <= 32) labudde_levels_team<NW, 1, 32>(M.hb, Q, Lr, Lr + 128, E, NTL, BS, warp, lane, 0);
+    else labudde_levels_team<NW, 1, 65>(M.hb, Q, Lr, Lr + 128, E, NTL, BS, warp, lane, 0);
+#ifdef LHAF_V5_TIMING
+    if (threadIdx.x == 0) atomicAdd(&g_v5_phase[3], (unsigned long long)clock64());
+#endif
+    if (warp == 0) {
+      const double2 *cB = Q;
+      const double2 *cM = D.loops ? Q + BS : Q;
+      double2 *scr = Q + (E + 1) * BS;
+      if (n + 2 <= 32) g = series<1>(cM, cB, n, NTL, D.loops, scr, lane);
+      else if (n + 2 <= 64) g = series<2>(cM, cB, n, NTL, D.loops, scr, lane);
+      else g = series<5>(cM, cB, n, NTL, D.loops, scr, lane);
+    }
+  } else {
+    const int QW = (E + 1) * BS;
+    double2 *Qh = M.u1, *Ql = Qh + QW;
+    double2 *scr = Ql + QW;                 // 6 (n + 2)
+    double2 *Lh = scr + 6 * (n + 2), *Ll = Lh + 128, *Th = Ll + 128, *Tl = Th + 2 * NW;
+    if (NTL <= 32) dd::labudde_levels_team<NW, 1, 32>(M.hb, Qh, Ql, Lh, Ll, Th, Tl, E, NTL, BS, warp, lane, 0);
+    else dd::labudde_levels_team<NW, 1, 65>(M.hb, Qh, Ql, Lh, Ll, Th, Tl, E, NTL, BS, warp, lane, 0);
+    if (warp == 0) {
+      const int o = D.loops ? BS : 0;
+      g = dd::series(Qh + o, Ql + o, Qh, Ql, n, NTL, D.loops, scr, lane);
+    }
   }
   __syncthreads();  // shared memory is reused by the next term
   return g;
 }
 
-template <int NW, int C0, int C1, int C2, int C3, int MINB>
+template <int NW, int C0, int C1, int C2, int C3, int MINB, bool PREC>
 __global__ void __launch_bounds__(32 * NW, MINB)
 sieve_v5(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
   extern __shared__ double2 smem[];
@@ -441,7 +457,7 @@ sieve_v5(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
     if (u >= uend) break;
     const PatDesc P = J.descs[find_pattern(J, u)];
     const Pattern D = pattern_of(P);
-    const Mem M = carve<NW>(smem, D.E, D.NTL, D.n);
+    const Mem M = carve<NW, PREC>(smem, D.E, D.NTL, D.n);
     const uint64_t tb = (u - P.unit_begin) * P.chunk;
     const uint64_t te = min(tb + P.chunk, P.T_eval);
     if (threadIdx.x < 6) s_acc[threadIdx.x] = 0.0;
@@ -451,7 +467,7 @@ sieve_v5(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
       V5_T0()
       team_reduce<NW, C0, C1, C2, C3>(P, D, J, t, M, warp, lane, sign, weight);
       V5_T1()
-      const double2 g = team_tail<NW>(D, M, warp, lane);
+      const double2 g = team_tail<NW, PREC>(D, M, warp, lane);
       V5_T2()
       if (threadIdx.x == 0) {
         const double sw = sign * weight;
@@ -471,7 +487,7 @@ sieve_v5(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
 }
 
 // g(t) (unweighted) of pattern 0 for a list of term indices; one CTA per index at a time.
-template <int NW, int C0, int C1, int C2, int C3, int MINB>
+template <int NW, int C0, int C1, int C2, int C3, int MINB, bool PREC>
 __global__ void __launch_bounds__(32 * NW, MINB)
 terms_v5(JobDev J, const uint64_t *ts, int nt, double2 *g_out, int team_words) {
   extern __shared__ double2 smem[];
@@ -480,12 +496,12 @@ terms_v5(JobDev J, const uint64_t *ts, int nt, double2 *g_out, int team_words) {
   __syncthreads();
   const PatDesc P = J.descs[0];
   const Pattern D = pattern_of(P);
-  const Mem M = carve<NW>(smem, D.E, D.NTL, D.n);
+  const Mem M = carve<NW, PREC>(smem, D.E, D.NTL, D.n);
   for (int i = blockIdx.x; i < nt; i += gridDim.x) {
     int sign;
     double weight;
     team_reduce<NW, C0, C1, C2, C3>(P, D, J, ts[i], M, warp, lane, sign, weight);
-    const double2 g = team_tail<NW>(D, M, warp, lane);
+    const double2 g = team_tail<NW, PREC>(D, M, warp, lane);
     if (threadIdx.x == 0) g_out[i] = g;
   }
 }
@@ -494,11 +510,12 @@ template <int NW, int C0, int C1, int C2, int C3, int MINB>
 struct Inst {
   static constexpr int EMAX = 16 * NW < 8 * C0 ? 16 * NW : 8 * C0;
   static constexpr int THREADS = 32 * NW;
+  template <bool PREC>
   static cudaError_t sieve(const JobDev &job, int E, int NTL, int n, uint64_t ubeg, uint64_t uend,
                            int num_sms, cudaStream_t s) {
-    const int tw = Shape<NW>::words(E, NTL, n);
+    const int tw = Shape<NW>::words(E, NTL, n, PREC);
     const size_t smem = (size_t)tw * sizeof(double2);
-    auto *kern = sieve_v5<NW, C0, C1, C2, C3, MINB>;
+    auto *kern = sieve_v5<NW, C0, C1, C2, C3, MINB, PREC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
@@ -515,11 +532,12 @@ struct Inst {
     kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw);
     return cudaGetLastError();
   }
+  template <bool PREC>
   static cudaError_t terms(const JobDev &job, int E, int NTL, int n, const uint64_t *t, int nt,
                            double2 *g_out, cudaStream_t s) {
-    const int tw = Shape<NW>::words(E, NTL, n);
+    const int tw = Shape<NW>::words(E, NTL, n, PREC);
     const size_t smem = (size_t)tw * sizeof(double2);
-    auto *kern = terms_v5<NW, C0, C1, C2, C3, MINB>;
+    auto *kern = terms_v5<NW, C0, C1, C2, C3, MINB, PREC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int grid = nt < 1184 ? nt : 1184;
@@ -531,6 +549,7 @@ struct Inst {
 // <warps, positions per lane in the four phases, CTAs per SM>; 16 rows per warp
 using I64 = Inst<4, 8, 6, 4, 2, 2>;  // 49 <= E <= 64 (cfg4: E = 61): 128 threads, 2 CTAs / SM
 using I48 = Inst<3, 6, 4, 2, 1, 4>;  // 33 <= E <= 48 (cfg5: E = 48): 96 threads, 4 CTAs / SM
+using I32 = Inst<2, 4, 3, 2, 1, 4>;  //       E <= 32 (precise mode; v3 is the fast path there)
 
 }  // namespace v5
 
@@ -543,25 +562,34 @@ extern "C" int lhaf_debug_v5_phase(unsigned long long *out4) {
 }
 #endif
 
-int v5_supported(int e_max) { return e_max > 32 && e_max <= 64; }
+int v5_supported(int e_max) { return e_max >= 1 && e_max <= 64; }
 
 cudaError_t launch_sieve_v5(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t ubeg,
-                            uint64_t uend, int num_sms, cudaStream_t s) {
+                            uint64_t uend, int num_sms, cudaStream_t s, int prec) {
   if (uend <= ubeg) return cudaSuccess;
   cudaError_t e = v5::ensure_inv();
   if (e != cudaSuccess) return e;
-  if (e_max <= v5::I48::EMAX) return v5::I48::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
-  if (e_max <= v5::I64::EMAX) return v5::I64::sieve(job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s);
+#define LHAF_V5_CALL(I, CALL) \
+  return prec ? v5::I::CALL<true> CALL##_ARGS : v5::I::CALL<false> CALL##_ARGS;
+#define sieve_ARGS (job, e_max, ntl_max, n_max, ubeg, uend, num_sms, s)
+  if (e_max <= v5::I32::EMAX) LHAF_V5_CALL(I32, sieve)
+  if (e_max <= v5::I48::EMAX) LHAF_V5_CALL(I48, sieve)
+  if (e_max <= v5::I64::EMAX) LHAF_V5_CALL(I64, sieve)
+#undef sieve_ARGS
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_terms_v5(const JobDev &job, int e_max, int ntl_max, int n_max, const uint64_t *t,
-                            int nt, double2 *g_out, cudaStream_t s) {
+                            int nt, double2 *g_out, cudaStream_t s, int prec) {
   if (nt <= 0) return cudaSuccess;
   cudaError_t e = v5::ensure_inv();
   if (e != cudaSuccess) return e;
-  if (e_max <= v5::I48::EMAX) return v5::I48::terms(job, e_max, ntl_max, n_max, t, nt, g_out, s);
-  if (e_max <= v5::I64::EMAX) return v5::I64::terms(job, e_max, ntl_max, n_max, t, nt, g_out, s);
+#define terms_ARGS (job, e_max, ntl_max, n_max, t, nt, g_out, s)
+  if (e_max <= v5::I32::EMAX) LHAF_V5_CALL(I32, terms)
+  if (e_max <= v5::I48::EMAX) LHAF_V5_CALL(I48, terms)
+  if (e_max <= v5::I64::EMAX) LHAF_V5_CALL(I64, terms)
+#undef terms_ARGS
+#undef LHAF_V5_CALL
   return cudaErrorInvalidValue;
 }
 
