@@ -169,6 +169,23 @@ lhaf_status lhaf_rpt_et(const double *A, const double *gamma, const int32_t *rep
 lhaf_status lhaf_gbs_prob(const double *sigma, const double *alpha, int32_t M, const int32_t *n,
                           int32_t pure, double out[2]);
 
+/* Gaussian-state constructor: the covariance sigma (2M*2M c128)
+ * and mean alpha (2M c128), in lhaf_gbs_prob's basis and convention, of M single-mode squeezed
+ * vacua (squeezing r_i, real, phase 0), pure loss per input mode (transmission eta_i in [0, 1];
+ * eta = NULL: lossless), the interferometer a -> U a (U: M*M c128, unitary to 1e-10) and a
+ * displacement beta of the output modes (M c128; NULL: none):
+ *   sigma_0 per mode = [[sinh^2 r + 1/2, -cosh r sinh r], [-cosh r sinh r, sinh^2 r + 1/2]],
+ *   loss sigma <- sqrt(E) sigma sqrt(E) + (I - E)/2, then S sigma S^dag, S = diag(U, U*),
+ *   alpha = (beta, conj(beta)).
+ * Host arithmetic; caller-owned outputs written only on LHAF_OK.  Errors: LHAF_E_ARG (null
+ * pointer, M outside [1, 2048], r not finite, eta outside [0, 1], U not unitary). */
+lhaf_status lhaf_gbs_state(const double *U, const double *r, const double *eta, const double *beta,
+                           int32_t M, double *sigma, double *alpha);
+/* P(n) of that state in one call: lhaf_gbs_state then lhaf_gbs_prob (the pure half-size form
+ * when every eta_i = 1).  out[0] = P, out[1] = imaginary residue.  Errors as the two calls. */
+lhaf_status lhaf_gbs_prob_state(const double *U, const double *r, const double *eta,
+                                const double *beta, int32_t M, const int32_t *n, double out[2]);
+
 /* The ingredients of lhaf_gbs_prob without a device: A (2M*2M c128), gamma (2M c128) and the
  * prefactor exp(-alpha^dag sigma_Q^{-1} alpha / 2) / sqrt(det sigma_Q) (out_pref: re, im).
  * Caller-owned outputs, written only on LHAF_OK.  Errors as lhaf_gbs_prob. */

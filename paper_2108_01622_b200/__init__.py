@@ -73,6 +73,8 @@ def _load() -> ctypes.CDLL:
         "lhaf_rpt_cutoff": ([dp, dp, ip, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, dp]),
         "lhaf_gbs_matrices": ([dp, dp, ctypes.c_int32, dp, dp, dp]),
         "lhaf_gbs_prob": ([dp, dp, ctypes.c_int32, ip, ctypes.c_int32, dp]),
+        "lhaf_gbs_state": ([dp, dp, vp, vp, ctypes.c_int32, dp, dp]),
+        "lhaf_gbs_prob_state": ([dp, dp, vp, vp, ctypes.c_int32, ip, dp]),
         "lhaf_ips_prob": ([dp, dp, ctypes.c_int32, ip, dp]),
         "lhaf_rpt_et": ([dp, dp, ip, ctypes.c_int32, dp]),
         "lhaf_rpt_multigamma": ([dp, dp, ctypes.c_int32, ip, ctypes.c_int32, dp]),
@@ -137,7 +139,8 @@ def reload_library():
 
 # every symbol include/lhaf.h declares (checked by tests/test_host.py::test_library_exports_every_declared_symbol)
 EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed", "lhaf_rpt_cutoff",
-            "lhaf_gbs_matrices", "lhaf_gbs_prob", "lhaf_ips_prob", "lhaf_rpt_et",
+            "lhaf_gbs_matrices", "lhaf_gbs_prob", "lhaf_gbs_state", "lhaf_gbs_prob_state",
+            "lhaf_ips_prob", "lhaf_rpt_et",
             "lhaf_rpt_multigamma",
             "lhaf_rpt_batch_dev", "lhaf_job_create", "lhaf_job_info_get", "lhaf_job_reset",
             "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_reset_range", "lhaf_job_allreduce_range",
@@ -232,6 +235,39 @@ def lhaf_gbs_prob(sigma, alpha, n, pure: bool = False) -> complex:
     sigma, alpha, n = _c128(sigma), _c128(alpha), _i32(n)
     out = np.zeros(2)
     _check(_lib.lhaf_gbs_prob(_dp(sigma), _dp(alpha), n.shape[0], _ip(n), 1 if pure else 0, _dp(out)))
+    return complex(out[0], out[1])
+
+
+def _opt_ptr(x, dtype):
+    if x is None:
+        return None, None
+    arr = np.ascontiguousarray(np.asarray(x, dtype=dtype))
+    return arr, arr.ctypes.data
+
+
+def lhaf_gbs_state(U, r, eta=None, beta=None):
+    """(sigma, alpha) of squeezers r -> pure loss eta -> U -> displacement beta."""
+    U = _c128(U)
+    M = U.shape[0]
+    r = np.ascontiguousarray(np.broadcast_to(np.asarray(r, float), (M,)))
+    e_arr, e_ptr = _opt_ptr(None if eta is None else np.broadcast_to(np.asarray(eta, float), (M,)), np.float64)
+    b_arr, b_ptr = _opt_ptr(beta, np.complex128)
+    sig = np.zeros((2 * M, 2 * M), np.complex128)
+    al = np.zeros(2 * M, np.complex128)
+    _check(_lib.lhaf_gbs_state(_dp(U), _dp(r), e_ptr, b_ptr, M, _dp(sig), _dp(al)))
+    return sig, al
+
+
+def lhaf_gbs_prob_state(U, r, n, eta=None, beta=None) -> complex:
+    """P(n) of the state of lhaf_gbs_state in one call."""
+    U = _c128(U)
+    M = U.shape[0]
+    r = np.ascontiguousarray(np.broadcast_to(np.asarray(r, float), (M,)))
+    e_arr, e_ptr = _opt_ptr(None if eta is None else np.broadcast_to(np.asarray(eta, float), (M,)), np.float64)
+    b_arr, b_ptr = _opt_ptr(beta, np.complex128)
+    nn = _i32(n)
+    out = np.zeros(2)
+    _check(_lib.lhaf_gbs_prob_state(_dp(U), _dp(r), e_ptr, b_ptr, M, _ip(nn), _dp(out)))
     return complex(out[0], out[1])
 
 

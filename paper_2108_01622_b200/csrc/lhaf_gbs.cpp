@@ -3,6 +3,7 @@
 // P:322-334), and the MIS proposal probability Q(n | B, alpha).  Host arithmetic on the 2M x 2M covariance (one LU per state: sigma_Q^{-1} and
 // det sigma_Q), then ONE device loop hafnian through the C-ABI (lhaf_rpt_mixed, or lhaf_rpt on
 // the half-size B_n for pure states).  Product code: shares nothing with oracle/.
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -93,9 +94,93 @@ lhaf_status gbs_matrices(const double *sigma, const double *alpha, int M, std::v
   return LHAF_OK;
 }
 
+// Covariance and mean of the Gaussian state prepared by M single-mode squeezers (r_i), pure loss
+// per input mode (transmission eta_i), the interferometer a -> U a and a displacement beta of the
+// output modes (App. A of SURVEY; reading C12 for the basis and sign conventions):
+//   input  sigma_0 = [[(sinh^2 r + 1/2) I, -cosh r sinh r], [-cosh r sinh r, (sinh^2 r + 1/2) I]]
+//          per mode in the basis (a_1..a_M, a_1^dag..a_M^dag) (sigma_ij = <a_i a_j^dag + a_j^dag a_i>/2);
+//   loss   sigma <- sqrt(E) sigma sqrt(E) + (I - E)/2,  E = diag(eta, eta);
+//   U      sigma <- S sigma S^dag,  S = diag(U, U*);   mean alpha = (beta, conj(beta)).
+void gbs_state(const double *U, const double *r, const double *eta, const double *beta, int M,
+               std::vector<cd> &sig, std::vector<cd> &alpha) {
+  const int n = 2 * M;
+  std::vector<cd> s0((size_t)n * n, 0.0);
+  for (int i = 0; i < M; ++i) {
+    const double ch = std::cosh(r[i]), sh = std::sinh(r[i]);
+    const double e = eta ? eta[i] : 1.0, se = std::sqrt(e);
+    s0[(size_t)i * n + i] = s0[(size_t)(i + M) * n + i + M] = e * (sh * sh + 0.5) + 0.5 * (1.0 - e);
+    s0[(size_t)i * n + i + M] = s0[(size_t)(i + M) * n + i] = -se * se * ch * sh;
+  }
+  // S sigma_0 S^dag with S = diag(U, U*)
+  auto Sij = [&](int a, int b) -> cd {  // S[a][b]
+    if (a < M && b < M) return cd(U[2 * ((size_t)a * M + b)], U[2 * ((size_t)a * M + b) + 1]);
+    if (a >= M && b >= M) return std::conj(cd(U[2 * ((size_t)(a - M) * M + b - M)], U[2 * ((size_t)(a - M) * M + b - M) + 1]));
+    return cd(0.0);
+  };
+  std::vector<cd> t((size_t)n * n, 0.0);  // S sigma_0
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b) {
+      cd acc = 0.0;
+      for (int c = 0; c < n; ++c) acc += Sij(a, c) * s0[(size_t)c * n + b];
+      t[(size_t)a * n + b] = acc;
+    }
+  sig.assign((size_t)n * n, 0.0);
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b) {
+      cd acc = 0.0;
+      for (int c = 0; c < n; ++c) acc += t[(size_t)a * n + c] * std::conj(Sij(b, c));
+      sig[(size_t)a * n + b] = acc;
+    }
+  alpha.assign(n, 0.0);
+  for (int i = 0; i < M; ++i) {
+    const cd b = beta ? cd(beta[2 * i], beta[2 * i + 1]) : cd(0.0);
+    alpha[i] = b;
+    alpha[i + M] = std::conj(b);
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+lhaf_status lhaf_gbs_state(const double *U, const double *r, const double *eta, const double *beta,
+                           int32_t M, double *sigma, double *alpha) {
+  if (!U || !r || !sigma || !alpha) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "null pointer");
+  if (M < 1 || M > 2048) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "bad mode count");
+  for (int i = 0; i < M; ++i) {
+    if (!std::isfinite(r[i])) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "squeezing not finite");
+    if (eta && !(eta[i] >= 0.0 && eta[i] <= 1.0))
+      return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "transmission outside [0, 1]");
+  }
+  // U must be unitary (to 1e-10): the constructor describes a lossless interferometer
+  double dev = 0.0;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < M; ++j) {
+      cd acc = 0.0;
+      for (int c = 0; c < M; ++c)
+        acc += cd(U[2 * ((size_t)i * M + c)], U[2 * ((size_t)i * M + c) + 1]) *
+               std::conj(cd(U[2 * ((size_t)j * M + c)], U[2 * ((size_t)j * M + c) + 1]));
+      dev = std::max(dev, std::abs(acc - ((i == j) ? cd(1.0) : cd(0.0))));
+    }
+  if (dev > 1e-10) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "U is not unitary");
+  std::vector<cd> sg, al;
+  gbs_state(U, r, eta, beta, M, sg, al);
+  for (size_t i = 0; i < sg.size(); ++i) { sigma[2 * i] = sg[i].real(); sigma[2 * i + 1] = sg[i].imag(); }
+  for (size_t i = 0; i < al.size(); ++i) { alpha[2 * i] = al[i].real(); alpha[2 * i + 1] = al[i].imag(); }
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_gbs_prob_state(const double *U, const double *r, const double *eta,
+                                const double *beta, int32_t M, const int32_t *n, double out[2]) {
+  if (!n || !out) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "null pointer");
+  if (M < 1 || M > 2048) return (lhaf_status)lhaf::set_error(LHAF_E_ARG, "bad mode count");
+  std::vector<double> sg((size_t)8 * M * M), al((size_t)4 * M);
+  lhaf_status s = lhaf_gbs_state(U, r, eta, beta, M, sg.data(), al.data());
+  if (s != LHAF_OK) return s;
+  bool pure = true;  // no loss: a pure state, the half-size |lhaf(B_n)|^2 form applies
+  for (int i = 0; eta && i < M; ++i) pure = pure && eta[i] == 1.0;
+  return lhaf_gbs_prob(sg.data(), al.data(), M, n, pure ? 1 : 0, out);
+}
 
 lhaf_status lhaf_gbs_matrices(const double *sigma, const double *alpha, int32_t M, double *A,
                               double *gamma, double out_pref[2]) {

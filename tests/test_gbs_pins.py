@@ -107,3 +107,34 @@ def test_oracle_ips_sum_rule(orc):
     al = G.complex_gaussian(2, 0.3, rng)
     tot = sum(orc.ips_prob(B, al, [i, j]) for i in range(9) for j in range(9) if i + j <= 8)
     assert 1.0 - 2e-5 < tot <= 1.0 + 1e-12, tot   # tail beyond |n| = 8: 8.5e-6
+
+
+def test_product_state_constructor(lib):
+    # lhaf_gbs_state (product, host arithmetic) against the closed forms of P:301-313: a single
+    # squeezed mode has sigma = [[sinh^2 r + 1/2, -cosh r sinh r], [., sinh^2 r + 1/2]]; pure
+    # states have det(sigma) = 4^-M; pure loss mixes with vacuum (sigma -> eta sigma + (1-eta)/2);
+    # the interferometer preserves the mean photon number tr(sigma)/2 - M/2; and it agrees with
+    # the test-input generator gbs_inputs.gaussian_state (written independently) to rounding
+    r = 0.8
+    sig, al = lib.lhaf_gbs_state(np.eye(1), [r])
+    want = np.array([[np.sinh(r) ** 2 + 0.5, -np.cosh(r) * np.sinh(r)],
+                     [-np.cosh(r) * np.sinh(r), np.sinh(r) ** 2 + 0.5]])
+    assert np.abs(sig - want).max() <= 1e-15 and np.abs(al).max() == 0
+    sig_l, _ = lib.lhaf_gbs_state(np.eye(1), [r], eta=[0.3])
+    assert np.abs(sig_l - (0.3 * want + 0.35 * np.eye(2))).max() <= 1e-15
+    rng = G.rng_for(2101)
+    M = 5
+    U = G.haar_unitary(M, rng)
+    rs = rng.uniform(0.1, 0.9, M)
+    sig, al = lib.lhaf_gbs_state(U, rs, beta=G.complex_gaussian(M, 0.3, rng))
+    assert abs(np.linalg.det(sig) - 4.0 ** -M) <= 1e-12 * 4.0 ** -M
+    assert abs(np.trace(sig).real / 2 - M / 2 - np.sum(np.sinh(rs) ** 2)) <= 1e-12
+    eta = rng.uniform(0.2, 1.0, M)
+    beta = G.complex_gaussian(M, 0.4, rng)
+    s1, a1 = lib.lhaf_gbs_state(U, rs, eta=eta, beta=beta)
+    s2, a2 = G.gaussian_state(U, rs, eta, beta)
+    assert np.abs(s1 - s2).max() <= 1e-13 and np.abs(a1 - a2).max() == 0
+    with pytest.raises(lib.LhafError):
+        lib.lhaf_gbs_state(2 * U, rs)                  # not unitary
+    with pytest.raises(lib.LhafError):
+        lib.lhaf_gbs_state(U, rs, eta=np.full(M, 1.5))  # transmission > 1

@@ -86,3 +86,31 @@ def test_ips_prob_vs_oracle(lib, orc):
     a2 = G.complex_gaussian(2, 0.3, rng)
     tot = sum(lib.lhaf_ips_prob(B2, a2, [i, j]) for i in range(11) for j in range(11) if i + j <= 10)
     assert 1.0 - 1e-5 < tot <= 1.0 + 1e-12, tot   # tail beyond |n| = 10: 2.8e-6
+
+
+def test_gbs_prob_state_vs_oracle_and_closed_forms(lib, orc):
+    # (U, r, eta, beta) -> P(n) in one product call, against the oracle's
+    # gbs_prob on the independently generated state, and the squeezed-vacuum / Poisson closed forms
+    rng = G.rng_for(2201)
+    M = 4
+    U = G.haar_unitary(M, rng)
+    rs = [0.6, 0.4, 0.5, 0.3]
+    eta = [0.7, 0.9, 0.8, 0.6]
+    beta = G.complex_gaussian(M, 0.3, rng)
+    sig, al = G.gaussian_state(U, np.array(rs), np.array(eta), beta)
+    for n in ([0, 0, 0, 0], [2, 1, 0, 1], [1, 1, 1, 1], [3, 0, 2, 0]):
+        want = orc.gbs_prob(sig, al, n)
+        got = lib.lhaf_gbs_prob_state(U, rs, n, eta=eta, beta=beta)
+        assert rel(got.real, want.real) <= 1e-10, (n, got, want)
+    for n in ([1, 0, 2, 0], [2, 2, 0, 1]):  # lossless: the pure half-size path
+        sig, al = G.gaussian_state(U, np.array(rs), 1.0, beta)
+        assert rel(lib.lhaf_gbs_prob_state(U, rs, n, beta=beta).real, orc.gbs_prob(sig, al, n).real) <= 1e-10
+    r = 0.7
+    t = math.tanh(r)
+    for k in range(6):
+        want = t ** (2 * k) * math.factorial(2 * k) / (4 ** k * math.factorial(k) ** 2 * math.cosh(r))
+        assert rel(lib.lhaf_gbs_prob_state(np.eye(1), [r], [2 * k]).real, want) <= 1e-12
+    b = 0.9 - 0.4j
+    for n in range(8):
+        want = math.exp(-abs(b) ** 2) * abs(b) ** (2 * n) / math.factorial(n)
+        assert rel(lib.lhaf_gbs_prob_state(np.eye(1), [0.0], [n], beta=[b]).real, want) <= 1e-12
