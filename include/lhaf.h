@@ -49,7 +49,8 @@ typedef enum {
                                or term count above the guard */
   LHAF_E_CUDA = 4,          /* CUDA runtime failure, or no device */
   LHAF_E_NCCL = 5,          /* NCCL failure (multi-rank only) */
-  LHAF_E_STATE = 6          /* library not initialised as required / inconsistent ranks */
+  LHAF_E_STATE = 6,         /* library not initialised as required / inconsistent ranks */
+  LHAF_E_INACCURATE = 7     /* results computed, but an error estimate exceeds the requested tolerance */
 } lhaf_status;
 
 #define LHAF_MAX_MODES 4096
@@ -129,6 +130,19 @@ lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t
  * LHAF_E_ARG for a bad mode / n_cut. */
 lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
                             int32_t k, int32_t mode, int32_t n_cut, double *out);
+/* The same, plus a per-count error estimate (the paper's accuracy mechanism: the
+ * sieve's error is its cancellation times the per-term rounding): err_est[j] = kappa_j * 2^-46
+ * with kappa_j = 2^{1-n} sum_t |term_t| / |lhaf_j| accumulated in the same pass (2^-46 ~ 64 eps
+ * is the FP64 per-term relative error scale measured for d <= 48).  The
+ * repeated-pair sieve cancels steeply with the count of one mode (tanh r = 0.6: kappa*eps ~ 2e-8,
+ * 8e-5, 1e-2, 1 at counts 4, 8, 12, 16 -- profiles/r01/cutoff_kappa_t0.6.txt), so high counts
+ * of a strongly squeezed mode are beyond FP64.  tol > 0: if some err_est[j] > tol, out and
+ * err_est are still written and LHAF_E_INACCURATE is returned (lhaf_last_error names the first
+ * such count); tol <= 0 never refuses.  err_est: n_cut + 1 doubles.  Other errors as
+ * lhaf_rpt_cutoff. */
+lhaf_status lhaf_rpt_cutoff_ex(const double *A, const double *gamma, const int32_t *reps_fixed,
+                               int32_t k, int32_t mode, int32_t n_cut, double tol, double *out,
+                               double *err_est);
 
 /* The same pattern under many loop vectors (the threshold chain rule's
  * sub-detector batching): out[2 g], out[2 g + 1] = lhaf of (A, gammas row g,

@@ -25,7 +25,7 @@ LIB_PATH = os.environ.get("LHAF_LIB_PATH") or os.path.join(_HERE, "liblhaf.so")
 LHAF_MAX_PAIRS = 64
 LHAF_OK = 0
 _STATUS = {0: "LHAF_OK", 1: "LHAF_E_ARG", 2: "LHAF_E_NOT_SYMMETRIC", 3: "LHAF_E_TOO_LARGE",
-           4: "LHAF_E_CUDA", 5: "LHAF_E_NCCL", 6: "LHAF_E_STATE"}
+           4: "LHAF_E_CUDA", 5: "LHAF_E_NCCL", 6: "LHAF_E_STATE", 7: "LHAF_E_INACCURATE"}
 
 
 class LhafError(RuntimeError):
@@ -71,6 +71,8 @@ def _load() -> ctypes.CDLL:
         "lhaf_rpt_batch": ([dp, dp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32, dp]),
         "lhaf_rpt_mixed": ([dp, dp, ip, ctypes.c_int32, dp]),
         "lhaf_rpt_cutoff": ([dp, dp, ip, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, dp]),
+        "lhaf_rpt_cutoff_ex": ([dp, dp, ip, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                ctypes.c_double, dp, dp]),
         "lhaf_gbs_matrices": ([dp, dp, ctypes.c_int32, dp, dp, dp]),
         "lhaf_gbs_prob": ([dp, dp, ctypes.c_int32, ip, ctypes.c_int32, dp]),
         "lhaf_gbs_state": ([dp, dp, vp, vp, ctypes.c_int32, dp, dp]),
@@ -139,6 +141,7 @@ def reload_library():
 
 # every symbol include/lhaf.h declares (checked by tests/test_host.py::test_library_exports_every_declared_symbol)
 EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_mixed", "lhaf_rpt_cutoff",
+            "lhaf_rpt_cutoff_ex",
             "lhaf_gbs_matrices", "lhaf_gbs_prob", "lhaf_gbs_state", "lhaf_gbs_prob_state",
             "lhaf_ips_prob", "lhaf_rpt_et",
             "lhaf_rpt_multigamma",
@@ -301,6 +304,17 @@ def lhaf_rpt_cutoff(A, gamma, reps_fixed, mode: int, n_cut: int) -> np.ndarray:
     out = np.zeros(2 * (n_cut + 1))
     _check(_lib.lhaf_rpt_cutoff(_dp(A), _dp(gamma), _ip(reps), reps.shape[0], mode, n_cut, _dp(out)))
     return out[0::2] + 1j * out[1::2]
+
+
+def lhaf_rpt_cutoff_ex(A, gamma, reps_fixed, mode: int, n_cut: int, tol: float = 0.0):
+    """lhaf_rpt_cutoff plus per-count error estimates kappa_j * 2^-46; with tol > 0 raises
+    LhafError (status LHAF_E_INACCURATE) when an estimate exceeds tol.  Returns (values, err)."""
+    A, gamma, reps = _c128(A), _c128(gamma), _i32(reps_fixed)
+    out = np.zeros(2 * (n_cut + 1))
+    err = np.zeros(n_cut + 1)
+    _check(_lib.lhaf_rpt_cutoff_ex(_dp(A), _dp(gamma), _ip(reps), reps.shape[0], mode, n_cut,
+                                   float(tol), _dp(out), _dp(err)))
+    return out[0::2] + 1j * out[1::2], err
 
 
 def lhaf_rpt_batch_dev(A_dev_ptr: int, gamma_dev_ptr: int, gamma_stride: int, reps_batch,

@@ -726,9 +726,39 @@ lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_s
   return s;
 }
 
+static lhaf_status cutoff_impl(const double *A, const double *gamma, const int32_t *reps_fixed,
+                               int32_t k, int32_t mode, int32_t n_cut, double *out, double *abs_out);
+
 lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t *reps_fixed,
                             int32_t k, int32_t mode, int32_t n_cut, double *out) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
+  return cutoff_impl(A, gamma, reps_fixed, k, mode, n_cut, out, nullptr);
+}
+
+lhaf_status lhaf_rpt_cutoff_ex(const double *A, const double *gamma, const int32_t *reps_fixed,
+                               int32_t k, int32_t mode, int32_t n_cut, double tol, double *out,
+                               double *err_est) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!err_est) return fail(LHAF_E_ARG, "null pointer argument");
+  std::vector<double> ab((size_t)n_cut + 1 > 0 ? (size_t)n_cut + 1 : 1);
+  lhaf_status s = cutoff_impl(A, gamma, reps_fixed, k, mode, n_cut, out, ab.data());
+  if (s != LHAF_OK) return s;
+  int worst = -1;
+  for (int c = 0; c <= n_cut; ++c) {
+    const double v = std::hypot(out[2 * c], out[2 * c + 1]);
+    // kappa = 2^{1-n} sum |term| / |lhaf| times the per-term error scale 2^-46 (~64 eps)
+    const double kap = v > 0.0 ? ab[c] / v : (ab[c] > 0.0 ? INFINITY : 1.0);
+    err_est[c] = kap * 0x1p-46;
+    if (tol > 0.0 && err_est[c] > tol && worst < 0) worst = c;
+  }
+  if (worst >= 0)
+    return fail(LHAF_E_INACCURATE, "count %d: estimated relative error %.2e > tol %.2e (sieve cancellation kappa %.2e)",
+                worst, err_est[worst], tol, err_est[worst] / 0x1p-46);
+  return LHAF_OK;
+}
+
+static lhaf_status cutoff_impl(const double *A, const double *gamma, const int32_t *reps_fixed,
+                               int32_t k, int32_t mode, int32_t n_cut, double *out, double *abs_out) {
   if (!A || !gamma || !reps_fixed || !out) return fail(LHAF_E_ARG, "null pointer argument");
   if (k < 1 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "k = %d out of range", k);
   if (mode < 0 || mode >= k) return fail(LHAF_E_ARG, "batched mode %d outside [0, %d)", mode, k);
@@ -787,7 +817,17 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
       memcpy(&reps[(size_t)c * k], reps_fixed, (size_t)k * sizeof(int32_t));
       reps[(size_t)c * k + mode] = c;
     }
-    return lhaf_rpt_batch(A, gamma, 0, reps.data(), k, n_cut + 1, out);
+    lhaf_job *jb = nullptr;
+    lhaf_status sb = job_create_impl(A, gamma, 0, reps.data(), k, n_cut + 1, 0, false, &jb);
+    if (sb != LHAF_OK) return sb;
+    std::vector<double> tmp(2 * (size_t)(n_cut + 1));
+    sb = evaluate(jb, tmp.data(), nullptr, 0);
+    if (sb == LHAF_OK && abs_out &&
+        cudaMemcpy(abs_out, jb->d_abs, (size_t)(n_cut + 1) * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      sb = fail(LHAF_E_CUDA, "reading the absolute sums failed");
+    job_free(jb);
+    if (sb == LHAF_OK) memcpy(out, tmp.data(), tmp.size() * sizeof(double));
+    return sb;
   }
   if (s != LHAF_OK) return s;
   // one sieve launch over both groups, then one finalize over n_cut + 1 virtual patterns
@@ -804,8 +844,10 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
   }
   PatDesc *d_vd = nullptr;
   double2 *d_o = nullptr;
+  double *d_ab = nullptr;
   cudaError_t e = upload(&d_vd, vd);
   if (e == cudaSuccess) e = dmalloc(&d_o, (n_cut + 1) * sizeof(double2));
+  if (e == cudaSuccess) e = dmalloc(&d_ab, (n_cut + 1) * sizeof(double));
   if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
   if (e == cudaSuccess)
     e = launch_sieve_cut_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, 0, j->units, g_ctx.num_sms, 0);
@@ -813,11 +855,13 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
     JobDev J = j->dev();
     J.descs = d_vd;
     J.npat = n_cut + 1;
-    e = launch_finalize(J, d_o, nullptr, 0);
+    e = launch_finalize(J, d_o, d_ab, 0);
   }
   if (e == cudaSuccess) e = cudaMemcpy(out, d_o, (n_cut + 1) * sizeof(double2), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && abs_out) e = cudaMemcpy(abs_out, d_ab, (n_cut + 1) * sizeof(double), cudaMemcpyDeviceToHost);
   dfree(d_vd);
   dfree(d_o);
+  dfree(d_ab);
   job_free(j);
   if (e != cudaSuccess) return fail(LHAF_E_CUDA, "cutoff job: %s", cudaGetErrorString(e));
   return LHAF_OK;

@@ -530,3 +530,24 @@ def test_per_term_parity_precise(precise, orc, which):
     print(f"P14 precise {which}: per-term median {np.median(per_term):.2e} max {per_term.max():.2e}; "
           f"max |err| / max |g| {scaled:.2e}")
     assert scaled <= 1e-12 and np.median(per_term) <= 3e-14, (which, scaled, np.median(per_term))
+
+
+def test_cutoff_error_estimates(lib, orc):
+    # lhaf_rpt_cutoff_ex: the per-count estimate kappa_j 2^-46 bounds the observed error against
+    # the oracle at every count, grows with the batched count, and tol refuses counts past it
+    rng = G.rng_for(5240)
+    k = 6
+    A = G.pure_B(G.haar_unitary(k, rng), 0.7)
+    g = G.complex_gaussian(k, 0.3, rng)
+    fixed = np.array([1, 1, 0, 1, 0, 1], np.int32)
+    vals, err = lib.lhaf_rpt_cutoff_ex(A, g, fixed, 2, 12)
+    assert np.allclose(vals, lib.lhaf_rpt_cutoff(A, g, fixed, 2, 12), rtol=0, atol=0)
+    for c in range(13):
+        reps = fixed.copy()
+        reps[2] = c
+        ref = orc.lhaf(A, g, reps)
+        assert rel(vals[c], ref) <= max(err[c], 1e-15), (c, rel(vals[c], ref), err[c])
+    assert err[12] > err[0]
+    with pytest.raises(lib.LhafError) as e:
+        lib.lhaf_rpt_cutoff_ex(A, g, fixed, 2, 12, tol=err[6] * 0.5)
+    assert e.value.status == 7
