@@ -145,12 +145,16 @@ lhaf_status lhaf_rpt_cutoff_ex(const double *A, const double *gamma, const int32
                                double *err_est);
 
 /* The same pattern under many loop vectors (the threshold chain rule's
- * sub-detector batching): out[2 g], out[2 g + 1] = lhaf of (A, gammas row g,
+ * sub-detector batching: "this does not change the eigenvalue calculation,
+ * so these calculations can be batched"): out[2 g], out[2 g + 1] = lhaf of (A, gammas row g,
  * reps), g < ngamma.  A: k*k c128, gammas: ngamma*k c128 row-major, reps: k int32, out:
- * 2 ngamma doubles.  One device job (the patterns share A, the plan and one sieve launch);
- * the paper's further saving -- one Hessenberg / characteristic polynomial per term shared by
- * all loop vectors -- is not implemented (each loop vector borders its own matrix).  Errors
- * as lhaf_rpt_batch. */
+ * 2 ngamma doubles.  Shared cubic step: per sieve term ONE Gauss-Hessenberg reduction of the
+ * loop-free M = C X_w (the loop vectors ride along as inert rows and columns), one La Budde
+ * (c_M) and one c_M^{-1/2}; per loop vector only the loop terms s_j = z'^T H^{j-1} y' by
+ * Hessenberg matvecs (O(n d^2)) and the exp series (O(n^2)) -- the v5 kernel's FLAG_MG path.
+ * Applies when d + ngamma <= 64, ngamma <= 16, FP64 mode and the automatic kernel choice;
+ * otherwise (or with LHAF_MULTIGAMMA_SEPARATE set) the pattern is evaluated once per loop vector
+ * in one batch job.  Errors as lhaf_rpt_batch. */
 lhaf_status lhaf_rpt_multigamma(const double *A, const double *gammas, int32_t ngamma,
                                 const int32_t *reps, int32_t k, double *out);
 

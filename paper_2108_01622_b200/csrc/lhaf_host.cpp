@@ -129,6 +129,7 @@ struct Plan {
   std::vector<int> p, q, eta;  // q = -1 for the phantom
   int eta_b = -1;              // >= 0: cutoff group (FLAG_CUT), the last pair is batched
   bool et = false;             // inclusion/exclusion (FLAG_ET): T_eval = T
+  int mg = 0;                  // > 0: gamma-batched evaluation of mg loop vectors (FLAG_MG)
 };
 
 lhaf_status make_plan(const int32_t *reps, int k, int mixed, Plan &P) {
@@ -325,7 +326,11 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   }
 
   // host view of gamma (loop flags are planned on the host)
-  const size_t gamma_len = gamma_stride ? (size_t)batch * gamma_stride : (size_t)kdim;
+  int mg_rows = 0;  // FLAG_MG: the gamma array holds G rows of the job's single pattern
+  if (plans_in)
+    for (const Plan &Pm : *plans_in) mg_rows = std::max(mg_rows, Pm.mg);
+  const size_t gamma_len = mg_rows ? (size_t)mg_rows * gamma_stride
+                                   : gamma_stride ? (size_t)batch * gamma_stride : (size_t)kdim;
   std::vector<double> gcopy;
   const double *ghost = gamma;
   if (on_device) {
@@ -371,7 +376,15 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     PatDesc &D = j->descs[b];
     memset(&D, 0, sizeof D);
     D.d = P.d; D.H = P.H; D.n = P.n; D.flags = 0;
-    {
+    if (P.mg > 0) {
+      // gamma-batched: M alone is reduced (no border); the loop vectors ride along (v5 MG)
+      D.flags |= FLAG_MG;
+      D.eta_b = P.mg;
+      if (P.H > 0) {
+        j->e_max = std::max(j->e_max, P.d);
+        j->ntl_max = std::max(j->ntl_max, std::min(P.n + 1, P.d + 1));
+      }
+    } else {
       bool loops = P.leftover >= 0;  // the phantom carries loop weight 1 (reading C7)
       const double *gb = ghost + 2 * (size_t)(gamma_stride ? (size_t)b * gamma_stride : 0);
       for (int h = 0; h < P.H && !loops; ++h)
@@ -403,7 +416,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     }
     D.units = (P.T_eval + D.chunk - 1) / D.chunk;
     unit += D.units;
-    part += D.units * (uint64_t)(P.eta_b >= 0 ? P.eta_b + 1 : 1);
+    part += D.units * (uint64_t)(P.mg > 0 ? P.mg : P.eta_b >= 0 ? P.eta_b + 1 : 1);
     j->terms += P.T_eval;
     j->d_max = std::max(j->d_max, P.d);
     j->n_max = std::max(j->n_max, P.n);
@@ -459,6 +472,11 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   j->variant = g_ctx.variant ? g_ctx.variant : choose_variant(j->e_max, j->n_max);
   j->prec = g_ctx.precision;
   if (j->prec) j->variant = 5;  // the precise tail lives in the v5 kernel (every E <= 64)
+  // inclusion/exclusion: excluded pairs are zero columns -- v5 deletes them per term (reduction
+  // at the term's own size), which is where ET's cost advantage comes from
+  bool any_et = false;
+  for (const auto &D : j->descs) any_et = any_et || (D.flags & FLAG_ET);
+  if (any_et && g_ctx.variant == 0 && v5_supported(j->e_max)) j->variant = 5;
   if (j->variant == 0 || (j->variant == 5 && !v5_supported(j->e_max))) j->variant = 3;
   if (j->prec && j->variant != 5) {
     job_free(j);
@@ -872,10 +890,51 @@ lhaf_status lhaf_rpt_multigamma(const double *A, const double *gammas, int32_t n
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   if (!A || !gammas || !reps || !out) return fail(LHAF_E_ARG, "null pointer argument");
   if (ngamma < 0 || k < 0 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "bad ngamma / k");
-  // one job: the same pattern once per loop vector (rows of gammas), one sieve launch
-  std::vector<int32_t> r((size_t)std::max(1, ngamma) * k);
-  for (int g = 0; g < ngamma; ++g) memcpy(&r[(size_t)g * k], reps, (size_t)k * sizeof(int32_t));
-  return lhaf_rpt_batch(A, gammas, k, r.data(), k, ngamma, out);
+  if (ngamma == 0) return LHAF_OK;
+  std::vector<Plan> plans(1);
+  lhaf_status s = make_plan(reps, k, 0, plans[0]);
+  if (s != LHAF_OK) return s;
+  const Plan &P0 = plans[0];
+  const bool shared = P0.H > 0 && P0.d + ngamma <= 64 && ngamma <= LHAF_MAX_GAMMA &&
+                      g_ctx.variant == 0 && g_ctx.precision == 0 && !getenv("LHAF_MULTIGAMMA_SEPARATE");
+  if (!shared) {
+    // the pattern once per loop vector in one batch job (G independent sieves)
+    std::vector<int32_t> r((size_t)ngamma * k);
+    for (int g = 0; g < ngamma; ++g) memcpy(&r[(size_t)g * k], reps, (size_t)k * sizeof(int32_t));
+    return lhaf_rpt_batch(A, gammas, k, r.data(), k, ngamma, out);
+  }
+  // one job, one pattern, FLAG_MG: one reduction per term shared by every loop vector
+  plans[0].mg = ngamma;
+  lhaf_job *j = nullptr;
+  s = job_create_impl(A, gammas, k, nullptr, k, 1, 0, false, &j, &plans);
+  if (s != LHAF_OK) return s;
+  std::vector<PatDesc> vd(ngamma);
+  const PatDesc &D = j->descs[0];
+  for (int g = 0; g < ngamma; ++g) {
+    memset(&vd[g], 0, sizeof(PatDesc));
+    vd[g].d = D.d;
+    vd[g].n = D.n;
+    vd[g].unit_begin = (uint64_t)D.part_base + (uint64_t)g * D.units;
+    vd[g].units = D.units;
+  }
+  PatDesc *d_vd = nullptr;
+  double2 *d_o = nullptr;
+  cudaError_t e = upload(&d_vd, vd);
+  if (e == cudaSuccess) e = dmalloc(&d_o, (size_t)ngamma * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
+  if (e == cudaSuccess) e = launch_sieve_mg_v5(j->dev(), j->d_max, ngamma, j->n_max, 0, j->units, g_ctx.num_sms, 0);
+  if (e == cudaSuccess) {
+    JobDev J = j->dev();
+    J.descs = d_vd;
+    J.npat = ngamma;
+    e = launch_finalize(J, d_o, nullptr, 0);
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, d_o, (size_t)ngamma * sizeof(double2), cudaMemcpyDeviceToHost);
+  dfree(d_vd);
+  dfree(d_o);
+  job_free(j);
+  if (e != cudaSuccess) return fail(LHAF_E_CUDA, "multigamma job: %s", cudaGetErrorString(e));
+  return LHAF_OK;
 }
 
 lhaf_status lhaf_rpt_et(const double *A, const double *gamma, const int32_t *reps, int32_t k,

@@ -35,6 +35,11 @@ constexpr uint32_t FLAG_CUT = 2u;
 // FLAG_ET: inclusion/exclusion over pair copies (ET) instead of the +-1 sieve:
 // w_h = eta_h - k_h, no halving, no 2^{-n} prefactor
 constexpr uint32_t FLAG_ET = 4u;
+// FLAG_MG: gamma-batched evaluation (lhaf_rpt_multigamma): eta_b holds the number G of loop
+// vectors (rows of the job's gamma array, stride kdim); partials per loop vector at
+// part_base + g * units + unit - unit_begin
+constexpr uint32_t FLAG_MG = 8u;
+constexpr int LHAF_MAX_GAMMA = 16;
 
 // Chunk partial: double-double complex sum of the unit's terms + sum |term|.
 struct Partial {
@@ -87,6 +92,9 @@ double v3_flops_per_term(int d, int n, bool loops);
 // Variant 5 (lhaf_v5.cu): 2-D register tile per lane, one barrier per column, 8 warps per team;
 // bordered sizes 33 <= E <= 64.  Same prep (launch_prep_bordered) and flop model as v3.
 int v5_supported(int e_max);
+// FLAG_MG jobs (one pattern, d + G <= 64, G <= LHAF_MAX_GAMMA)
+cudaError_t launch_sieve_mg_v5(const JobDev &job, int e_max, int g_max, int n_max, uint64_t unit_begin,
+                               uint64_t unit_end, int num_sms, cudaStream_t s);
 // prec = 1: the precise tail (double-double La Budde and series, lhaf_dd.cuh)
 cudaError_t launch_sieve_v5(const JobDev &job, int e_max, int ntl_max, int n_max, uint64_t unit_begin,
                             uint64_t unit_end, int num_sms, cudaStream_t s, int prec);

@@ -334,6 +334,71 @@ __device__ __forceinline__ double2 series(const double2 *cM, const double2 *cB, 
   return warp_sum2(gp);
 }
 
+// The two halves of series() for many loop vectors sharing one c_M (gamma-batched evaluation):
+// qhalf_coeffs writes Q = c_M^{-1/2} (degrees 0..n) to Qs once per term; exp_dot then gives, per
+// loop vector, g = sum_m Q_m E_{n-m} with E = exp(S/2), S = sum_{j>=1} s_j lam^j given directly
+// (s_j = z'^T H^{j-1} y' from the Krylov products).  One warp each; Es: n + 1 scratch.
+template <int NR>
+__device__ __forceinline__ void qhalf_coeffs(const double2 *cM, int n, int NTL, double2 *Qs, int lane) {
+  double2 qa[NR];
+  double md[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    md[r] = (double)(lane + 32 * r);
+    qa[r] = c0();
+  }
+  double jd = 0.0;
+  for (int j = 0; j <= n; ++j, jd += 1.0) {
+    const int lj = j & 31, rj = j >> 5;
+    double2 qs = qa[0];
+#pragma unroll
+    for (int r = 1; r < NR; ++r)
+      if (rj == r) qs = qa[r];
+    double2 qj = (j == 0) ? c1() : cscale(qs, -c_inv[j]);
+    qj = shfl2(qj, lj);
+    if (lane == lj) Qs[j] = qj;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int m = lane + 32 * r;
+      if (m > j && m <= n && m - j < NTL) qa[r] = cfma(cscale(cM[m - j], 0.5 * (md[r] + jd)), qj, qa[r]);
+    }
+  }
+  __syncwarp();
+}
+
+template <int NR>
+__device__ __forceinline__ double2 exp_dot(const double2 *Qs, const double2 *S, int n, double2 *Es,
+                                           int lane) {
+  double2 ea[NR];
+  double md[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    md[r] = (double)(lane + 32 * r);
+    ea[r] = c0();
+  }
+  double id = 0.0;
+  for (int i = 0; i <= n; ++i, id += 1.0) {
+    const int li = i & 31, ri = i >> 5;
+    double2 es = ea[0];
+#pragma unroll
+    for (int r = 1; r < NR; ++r)
+      if (ri == r) es = ea[r];
+    double2 ei = (i == 0) ? c1() : cscale(es, c_inv[i]);
+    ei = shfl2(ei, li);
+    if (lane == li) Es[i] = ei;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int m = lane + 32 * r;
+      // m E_m = 1/2 sum_{j=1}^{m} j S_j E_{m-j}: the term of E_i in lane m has j = m - i
+      if (m > i && m <= n) ea[r] = cfma(cscale(S[m - i], 0.5 * (md[r] - id)), ei, ea[r]);
+    }
+  }
+  __syncwarp();
+  double2 gp = c0();
+  for (int m = lane; m <= n; m += 32) gp = cfma(Qs[m], Es[n - m], gp);
+  return warp_sum2(gp);
+}
+
 // Blocked team La Budde (one barrier per BK rows).  Rows are processed in blocks of BK from
 // the bottom; block b = rows [jhi - BK + 1, jhi], jhi = E - 1 - b BK.  For row j of block b
 // the m-sum of S_j splits by source row s = j + m + 1:
@@ -538,10 +603,15 @@ __device__ __forceinline__ void labudde_levels(const double2 *hb, double2 *Q, in
 //   (c) team barrier.
 // After the last level the rows are finalised once more (and synchronised) for the series.
 // Q: [E + 1][BS]; L: [2][64]; tot: [2][NW]; hb, BS as labudde_levels.
+// QS: row stride of Q (default BS).  zmask: bit i set if H[i][i-1] = 0 (gamma-batched evaluation
+// keeps the true H: the terms of F_j[m] crossing a zero subdiagonal are dropped here instead of
+// being zeroed in the band).
 template <int NW, int TEAMS, int NTLMAX>
 __device__ __forceinline__ void labudde_levels_team(const double2 *hb, double2 *Q, double2 *L,
                                                     double2 *tot, int E, int NTL, int BS,
-                                                    int warp, int lane, int team) {
+                                                    int warp, int lane, int team, int QS = 0,
+                                                    uint64_t zmask = 0) {
+  if (QS == 0) QS = BS;
   constexpr int MT = NTLMAX / 2;  // m-terms per lane at most (m <= NTL - 2, half of them)
   const int i = warp * 16 + (lane >> 1), h = lane & 1;
   const bool ri = i < E;
@@ -549,8 +619,8 @@ __device__ __forceinline__ void labudde_levels_team(const double2 *hb, double2 *
   const int mx = ri ? E - 1 - i : 0;  // largest valid m of row i
   const double2 *F = hb + ci * BS + 1;
   const double2 hii = (ri && h == 0) ? F[0] : c0();
-  if (h == 0 && i <= E) Q[i * BS] = c1();  // monic
-  if (warp == 0 && lane == 0 && E >= NW * 16) Q[E * BS] = c1();
+  if (h == 0 && i <= E) Q[i * QS] = c1();  // monic
+  if (warp == 0 && lane == 0 && E >= NW * 16) Q[E * QS] = c1();
   team_sync<NW, TEAMS>(team);
   for (int t = 1; t < NTL; ++t) {
     const int pb = (t - 1) & 1, cb = t & 1;
@@ -560,7 +630,7 @@ __device__ __forceinline__ void labudde_levels_team(const double2 *hb, double2 *
 #pragma unroll
       for (int w = NW - 1; w > 0; --w)
         if (w > warp) Cw = cadd(Cw, tot[pb * NW + w]);
-      if (h == 0 && i <= E) Q[i * BS + t - 1] = (i < E && t - 1 <= E - i) ? cadd(L[pb * 64 + i], Cw) : c0();
+      if (h == 0 && i <= E) Q[i * QS + t - 1] = (i < E && t - 1 <= E - i) ? cadd(L[pb * 64 + i], Cw) : c0();
     }
     // (b) u_i[t]: the h-term from level t-1 (fresh: L + correction of the row's warp)
     double2 a = c0(), b = c0();
@@ -587,9 +657,9 @@ __device__ __forceinline__ void labudde_levels_team(const double2 *hb, double2 *
     for (int x = 0; x < MT; ++x) {
       const int m = 1 + h + 2 * x;
       if (2 * x + 1 > NTLMAX - 2) break;
-      const bool ok = m <= t - 1 && m <= mx;
+      const bool ok = m <= t - 1 && m <= mx && ((zmask >> (i + 1)) & ((1ull << m) - 1ull)) == 0;
       const double2 f = ok ? F[m] : c0();
-      const double2 q = Q[min(i + m + 1, E) * BS + max(t - m - 1, 0)];
+      const double2 q = Q[min(i + m + 1, E) * QS + max(t - m - 1, 0)];
       if (x % 4 == 0) a = cfms(f, q, a);
       else if (x % 4 == 1) b = cfms(f, q, b);
       else if (x % 4 == 2) c = cfms(f, q, c);
@@ -616,10 +686,10 @@ __device__ __forceinline__ void labudde_levels_team(const double2 *hb, double2 *
 #pragma unroll
       for (int w = NW - 1; w > 0; --w)
         if (w > warp) Cw = cadd(Cw, tot[pb * NW + w]);
-      if (h == 0 && i <= E) Q[i * BS + t - 1] = (i < E && t - 1 <= E - i) ? cadd(L[pb * 64 + i], Cw) : c0();
+      if (h == 0 && i <= E) Q[i * QS + t - 1] = (i < E && t - 1 <= E - i) ? cadd(L[pb * 64 + i], Cw) : c0();
     }
     if (warp == 0 && lane == 0 && E >= NW * 16) {
-      for (int tt = 1; tt < NTL; ++tt) Q[E * BS + tt] = c0();
+      for (int tt = 1; tt < NTL; ++tt) Q[E * QS + tt] = c0();
     }
   }
   team_sync<NW, TEAMS>(team);

@@ -110,9 +110,19 @@ struct St {
   double2 rs;       // my row's scale (1 / pivot if it was a pivot row)
   uint64_t live;    // indices with label > k (team-uniform)
   uint64_t livec;   // the live set at the last compaction (defines the positions)
+  uint64_t inert;   // gamma-batched evaluation: the loop-vector rows / columns (never pivots)
+  uint64_t zmask;   // bit k+1 set if H[k+1][k] = 0 (an exactly-zero pivot at step k)
   int Lc;           // popc(livec): positions >= Lc have no column
   int zl;           // 1 + the label after the latest zero subdiagonal (0: none)
   int buf;
+};
+
+// gamma-batched evaluation (FLAG_MG): the outputs of the reduction besides H
+struct MgOut {
+  double2 *Y, *Z;  // [G][YS]: y'_g = D^{-1} L y_g and z'_g = z_g L^{-1} D, indexed by label
+  int YS;
+  int base;        // E0: the first loop-vector index
+  uint64_t zmask;  // (out) zero subdiagonals of H
 };
 
 __device__ __forceinline__ int nth_bit(uint64_t m, int q) {  // position of the q-th set bit
@@ -172,7 +182,8 @@ __device__ __forceinline__ double rs8(double (&v)[8], int cg) {
 // Steps k in [k0, k1) of the reduction with CJ positions per lane (the tile prefix).
 template <int NW, int CJ, int CJF>
 __device__ __forceinline__ void steps(double2 (&A)[4][CJF], St &st, int k0, int k1, int E,
-                                      int NTL, const Mem &M, int warp, int lane) {
+                                      int NTL, int BS, const Mem &M, int warp, int lane,
+                                      const MgOut *mg = nullptr) {
   using Sh = Shape<NW>;
   const int cg = lane & 7, me = cg >> 1, im = cg & 1;
   const int rho0 = row_of(warp, lane, 0), rho = rho0 + me;
@@ -234,7 +245,7 @@ __device__ __forceinline__ void steps(double2 (&A)[4][CJF], St &st, int k0, int 
     const int nl = (rho == p) ? k + 1 : (st.label == k + 1 ? plabel : st.label);
     // finished column k: H[label][k] for rows with label <= k + 1 (band of width NTL)
     if (!im && nl <= k + 1 && k + 1 - nl < NTL)
-      hb[nl * (NTL + 1) + k + 1 - nl] = (nl < st.zl) ? c0() : cmul(st.rs, st.colv);
+      hb[nl * BS + k + 1 - nl] = (nl < st.zl && !mg) ? c0() : cmul(st.rs, st.colv);
     st.live &= ~(1ull << p);
     const double2 mm = (elim && cd && rho != p) ? cmul(st.colv, ip) : c0();
     double2 m[4];
@@ -269,8 +280,11 @@ __device__ __forceinline__ void steps(double2 (&A)[4][CJF], St &st, int k0, int 
     } else {
       st.colv = my_entry<CJ, CJF>(A, qp, lane);  // nothing to eliminate: column p as it stands
       st.zl = k + 1;                             // H[k+1][k] = 0
+      st.zmask |= 1ull << (k + 1);
     }
     st.label = nl;
+    if (mg && !im && rho < 64 && ((st.inert >> rho) & 1ull))  // z' entry of the column labelled k+1
+      mg->Z[(rho - mg->base) * mg->YS + k + 1] = st.colv;
   }
 }
 
@@ -281,7 +295,7 @@ template <int CJA, int CJB, int CJF>
 __device__ __forceinline__ void compact(double2 (&A)[4][CJF], St &st, double2 *wbuf, int warp,
                                         int lane) {
   const int rg = lane >> 3, cg = lane & 7;
-  const uint64_t lv = st.live;
+  const uint64_t lv = st.live | st.inert;  // the loop-vector columns keep their positions
   const int L = __popcll(lv);
   int np[CJA];
 #pragma unroll
@@ -310,14 +324,24 @@ __device__ __forceinline__ void compact(double2 (&A)[4][CJF], St &st, double2 *w
   st.Lc = L;
 }
 
+
 // a4-a6 of one term: decode, build, phased Hessenberg reduction into the band M.hb.
 // Widths (positions per lane) C0 > C1 > C2 > C3; a phase switches when the live columns fit.
-template <int NW, int C0, int C1, int C2, int C3>
-__device__ __forceinline__ void team_reduce(const PatDesc &P, const Pattern &D, const JobDev &J,
+// Zero-weight deletion: an index c whose column weight is 0 (w_h = 0: eta_h = 2 k_h in the sieve,
+// an excluded pair in inclusion/exclusion) has the column e_c in I - lam B, so det(I - lam B) is
+// the minor without row and column c (and the loop row z vanishes there too): such indices are
+// removed before the reduction -- the term is reduced at its own size E' (the paper's "z_i = 0
+// deletion").  Returns (E', NTL') of the term.
+template <int NW, int C0, int C1, int C2, int C3, bool MG = false>
+__device__ __forceinline__ int2 team_reduce(const PatDesc &P, const Pattern &D, const JobDev &J,
                                             uint64_t t, const Mem &M, int warp, int lane,
-                                            int &sign, double &weight) {
+                                            int &sign, double &weight, MgOut *mg = nullptr) {
   using Sh = Shape<NW>;
-  const int H = D.H, E = D.E, o = D.o, NTL = D.NTL;
+  const int H = D.H, E0 = D.E, o = D.o;
+  // MG: the band is the full H (row stride HS = E0 + 1) read through hb = Hf - 1 with BS = HS + 1
+  // (hb[j BS + 1 + m] = Hf[j HS + j + m] = H[j][j+m]), so every entry is written
+  const int BS = MG ? E0 + 2 : D.NTL + 1;
+  const int G = MG ? P.eta_b : 0;
   const int cg = lane & 7, im = cg & 1;
   const int rho0 = row_of(warp, lane, 0), rho = rho0 + (cg >> 1);
   // ---- a4: decode; ww[c] = weight of column c of B (1 for the border column)
@@ -326,64 +350,131 @@ __device__ __forceinline__ void team_reduce(const PatDesc &P, const Pattern &D, 
     __syncwarp();
     for (int c = lane; c < 64; c += 32) {
       const int j = c - o;
-      M.ww[c] = (c >= E) ? 0.0 : (j < 0) ? 1.0 : (double)M.wv[j < H ? j : j - H];
+      M.ww[c] = (c >= E0) ? 0.0 : (j < 0) ? 1.0 : (double)M.wv[j < H ? j : j - H];
     }
   }
   __syncthreads();
+  // kept indices (nonzero weight) and the term's own size
+  const uint64_t keep = ((uint64_t)__ballot_sync(LHAF_FULL, M.ww[lane + 32] != 0.0) << 32) |
+                        (uint64_t)__ballot_sync(LHAF_FULL, M.ww[lane] != 0.0);
+  const int E = __popcll(keep);
+  const int NTL = MG ? 64 : min(D.n + 1 + o, E + 1);  // MG: band condition always true
+  const int r0 = keep ? __ffsll((long long)keep) - 1 : 0;  // label 0: the first pivot column
   // ---- a5: tile of B = B0 diag(ww); position q = column q initially
   const double2 *B0 = J.cpool + P.mat_off;
   double2 A[4][C0];
 #pragma unroll
   for (int j = 0; j < C0; ++j) {
     const int c = cg + 8 * j;
-    const bool cok = c < E;
+    const bool cok = c < E0;
     const double w = cok ? M.ww[c] : 0.0;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      A[i][j] = (cok && rho0 + i < E) ? cscale(B0[(size_t)(rho0 + i) * E + c], w) : c0();
+      A[i][j] = (cok && rho0 + i < E0) ? cscale(B0[(size_t)(rho0 + i) * E0 + c], w) : c0();
+  }
+  if constexpr (MG) {
+    // loop vectors: y_g = v_g as column E0 + g, z_g = v_g X_w as row E0 + g (v_g[a] = gamma_g at
+    // the index list entry a; the phantom's loop weight is 1)
+    const int *rix = J.ipool + P.idx_off;
+    const double2 *gam = J.gamma + P.gamma_off;
+#pragma unroll
+    for (int j = 0; j < C0; ++j) {
+      const int c = cg + 8 * j;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = rho0 + i;
+        if (r < E0 && c >= E0 && c < E0 + G) {
+          const int ri = rix[r];
+          A[i][j] = ri < 0 ? c1() : gam[(size_t)(c - E0) * J.kdim + ri];
+        } else if (r >= E0 && r < E0 + G && c < E0) {
+          const int pc = c < H ? c + H : c - H;
+          const int ri = rix[pc];
+          const double2 v = ri < 0 ? c1() : gam[(size_t)(r - E0) * J.kdim + ri];
+          A[i][j] = cscale(v, M.ww[c]);
+        }
+      }
+    }
   }
   St st;
-  st.label = rho;
-  st.pos = rho < E ? rho : -1;
-  st.colv = rho < E ? cscale(B0[(size_t)rho * E], M.ww[0]) : c0();  // column 0: the first pivot column
+  const bool kept = rho < 64 && ((keep >> rho) & 1ull);
+  st.label = kept ? __popcll(keep & ((1ull << rho) - 1ull)) : 63;  // deleted rows: never pivots
+  st.pos = rho < E0 ? rho : -1;
+  const int r0c = (MG && rho >= E0) ? 0 : rho;  // (a loop-vector row reads its own tile below)
+  st.colv = kept ? cscale(B0[(size_t)r0c * E0 + r0], M.ww[r0]) : c0();  // the first pivot column
   st.rs = c1();
-  const uint64_t all = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
-  st.live = all & ~1ull;
+  const int ET = E0 + G;
+  const uint64_t all = ET >= 64 ? ~0ull : ((1ull << ET) - 1ull);
+  st.inert = MG ? (all & ~(E0 >= 64 ? ~0ull : ((1ull << E0) - 1ull))) : 0ull;
+  st.live = keep & ~(1ull << r0);
   st.livec = all;
-  st.Lc = E;
+  st.Lc = ET;
   st.zl = 0;
+  st.zmask = 0;
   st.buf = 0;
-  // ---- a6: phased reduction
-  const int kend = E >= 2 ? E - 2 : 0;
-  const int k1 = min(kend, max(0, E - 1 - 8 * C1));
-  const int k2 = max(k1, min(kend, max(0, E - 1 - 8 * C2)));
-  const int k3 = max(k2, min(kend, max(0, E - 1 - 8 * C3)));
+  if constexpr (MG) {
+    st.pos = rho < ET ? rho : -1;  // the loop-vector rows own (and zero) the kb entries of their columns
+    // the first pivot column's entry: B[row][r0] (a loop-vector row: z_g[r0])
+    const double2 e0 = my_entry<C0, C0>(A, r0, lane);
+    st.colv = (kept || (rho >= E0 && rho < ET)) ? e0 : c0();
+    if (!im && rho >= E0 && rho < ET) mg->Z[(rho - E0) * mg->YS] = st.colv;  // z'[label 0]
+  }
   double2 *wbuf = M.u1 + Sh::CMP + warp * 4 * 48;
-  steps<NW, C0, C0>(A, st, 0, k1, E, NTL, M, warp, lane);
+  if (E != E0) compact<C0, C0, C0>(A, st, wbuf, warp, lane);  // drop the deleted columns
+  // ---- a6: phased reduction (the loop-vector columns occupy G positions throughout)
+  const int kend = E >= 2 ? E - 2 : 0;
+  const int k1 = min(kend, max(0, E - 1 + G - 8 * C1));
+  const int k2 = max(k1, min(kend, max(0, E - 1 + G - 8 * C2)));
+  const int k3 = max(k2, min(kend, max(0, E - 1 + G - 8 * C3)));
+  const MgOut *mgp = MG ? mg : nullptr;
+  steps<NW, C0, C0>(A, st, 0, k1, E, NTL, BS, M, warp, lane, mgp);
   compact<C0, C1, C0>(A, st, wbuf, warp, lane);
-  steps<NW, C1, C0>(A, st, k1, k2, E, NTL, M, warp, lane);
+  steps<NW, C1, C0>(A, st, k1, k2, E, NTL, BS, M, warp, lane, mgp);
   compact<C1, C2, C0>(A, st, wbuf, warp, lane);
-  steps<NW, C2, C0>(A, st, k2, k3, E, NTL, M, warp, lane);
+  steps<NW, C2, C0>(A, st, k2, k3, E, NTL, BS, M, warp, lane, mgp);
   compact<C2, C3, C0>(A, st, wbuf, warp, lane);
-  steps<NW, C3, C0>(A, st, k3, kend, E, NTL, M, warp, lane);
+  steps<NW, C3, C0>(A, st, k3, kend, E, NTL, BS, M, warp, lane, mgp);
   // the last two columns: the carried one (label kend) and the last live index (label E-1)
   double2 *hb = M.hb;
-  const int BS = NTL + 1;
   if (E >= 2) {
     const int pl = __ffsll((long long)st.live) - 1;
     const int pos = __popcll(st.livec & ((1ull << pl) - 1ull));
     const double2 cl = my_entry<C3, C0>(A, pos, lane);
     if (!im) {
       const int lb = st.label;
-      if (lb < E && kend + 1 - lb < NTL) hb[lb * BS + kend + 1 - lb] = (lb < st.zl) ? c0() : cmul(st.rs, st.colv);
+      if (lb < E && kend + 1 - lb < NTL) hb[lb * BS + kend + 1 - lb] = (lb < st.zl && !MG) ? c0() : cmul(st.rs, st.colv);
       if (rho == pl) *M.beta = st.colv;  // H[E-1][E-2], not yet scaled to 1
-      if (lb < E && E - lb < NTL) hb[lb * BS + E - lb] = (lb < st.zl) ? c0() : cmul(st.rs, cl);
+      if (lb < E && E - lb < NTL) hb[lb * BS + E - lb] = (lb < st.zl && !MG) ? c0() : cmul(st.rs, cl);
+      if (MG && rho < 64 && ((st.inert >> rho) & 1ull)) mg->Z[(rho - E0) * mg->YS + E - 1] = cl;
+    }
+  } else if (E == 1 && !im && st.label == 0) {
+    hb[1] = st.colv;  // H[0][0] (a 1 x 1 term: the first pivot column is its only entry)
+  }
+  if constexpr (MG) {
+    // y'_g[label] = rs (L y_g)[row]: the loop-vector columns after all left updates
+    if (E >= 1) {
+      for (int gi = 0; gi < G; ++gi) {
+        const int q = __popcll(st.livec & ((1ull << (E0 + gi)) - 1ull));
+        const double2 y = my_entry<C3, C0>(A, q, lane);
+        if (!im && st.label < E) mg->Y[gi * mg->YS + st.label] = cmul(st.rs, y);
+      }
     }
   }
   __syncthreads();
-  // the last subdiagonal: scale column E-1 by it (rows above E-1)
-  if (E >= 2 && !im && st.label < E - 1 && E - st.label < NTL)
+  // the last subdiagonal: scale column E-1 by it (rows above E-1): the similarity diag(.., beta)
+  const bool beta_zero = E >= 2 && M.beta->x == 0.0 && M.beta->y == 0.0;
+  if (E >= 2 && !im && st.label < E - 1 && E - st.label < NTL && !(MG && beta_zero))
     hb[st.label * BS + E - st.label] = cmul(hb[st.label * BS + E - st.label], *M.beta);
+  if constexpr (MG) {  // the same similarity on the loop vectors: y'[E-1] / beta, z'[E-1] * beta
+    const double2 b = *M.beta;
+    const bool zb = (b.x == 0.0 && b.y == 0.0);  // an exactly zero last subdiagonal: no scaling
+    if (E >= 2 && threadIdx.x < G && !zb) {
+      const int gi = threadIdx.x;
+      mg->Y[gi * mg->YS + E - 1] = cmul(mg->Y[gi * mg->YS + E - 1], crecip(b));
+      mg->Z[gi * mg->YS + E - 1] = cmul(mg->Z[gi * mg->YS + E - 1], b);
+    }
+    mg->zmask = st.zmask | ((E >= 2 && zb) ? (1ull << (E - 1)) : 0ull);
+  }
+  return make_int2(E, MG ? min(D.n + 1, E + 1) : NTL);
 }
 
 #ifdef LHAF_V5_TIMING  // diagnostic builds: cycles of thread 0 in the reduction and the tail
@@ -406,8 +497,9 @@ __device__ unsigned long long g_v5_phase[4];
 // a7-a9 of one term: level-by-level team La Budde on the band (q rows in the reduction's
 // scratch, free by now), then the series in warp 0; PREC: both in double-double (lhaf_dd.cuh)
 template <int NW, bool PREC>
-__device__ __forceinline__ double2 team_tail(const Pattern &D, const Mem &M, int warp, int lane) {
-  const int n = D.n, E = D.E, NTL = D.NTL, BS = NTL + 1;
+__device__ __forceinline__ double2 team_tail(const Pattern &D, int2 en, const Mem &M, int warp,
+                                             int lane) {
+  const int n = D.n, E = en.x, NTL = en.y, BS = D.NTL + 1;
   double2 g = c0();
   if constexpr (!PREC) {
     double2 *Q = M.u1;
@@ -465,9 +557,9 @@ sieve_v5(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
       int sign = 1;
       double weight = 1.0;
       V5_T0()
-      team_reduce<NW, C0, C1, C2, C3>(P, D, J, t, M, warp, lane, sign, weight);
+      const int2 en = team_reduce<NW, C0, C1, C2, C3>(P, D, J, t, M, warp, lane, sign, weight);
       V5_T1()
-      const double2 g = team_tail<NW, PREC>(D, M, warp, lane);
+      const double2 g = team_tail<NW, PREC>(D, en, M, warp, lane);
       V5_T2()
       if (threadIdx.x == 0) {
         const double sw = sign * weight;
@@ -500,9 +592,156 @@ terms_v5(JobDev J, const uint64_t *ts, int nt, double2 *g_out, int team_words) {
   for (int i = blockIdx.x; i < nt; i += gridDim.x) {
     int sign;
     double weight;
-    team_reduce<NW, C0, C1, C2, C3>(P, D, J, ts[i], M, warp, lane, sign, weight);
-    const double2 g = team_tail<NW, PREC>(D, M, warp, lane);
+    const int2 en = team_reduce<NW, C0, C1, C2, C3>(P, D, J, ts[i], M, warp, lane, sign, weight);
+    const double2 g = team_tail<NW, PREC>(D, en, M, warp, lane);
     if (threadIdx.x == 0) g_out[i] = g;
+  }
+}
+
+// ================================================================ gamma-batched evaluation
+// (FLAG_MG; "only the diagonal entries ... change between
+// sub-detectors ... this does not change the eigenvalue calculation").  Per term ONE reduction of
+// the gamma-free M = C X_w (the loop vectors ride along as G inert columns y_g = v_g and G inert
+// rows z_g = v_g X_w: never pivots, they receive the same left / right updates and end as
+// y'_g = D^-1 L y_g, z'_g = z_g L^-1 D), ONE La Budde (c_M) and ONE c_M^{-1/2}; per loop vector
+// only the loop terms s_j = z'_g^T H^{j-1} y'_g (Hessenberg matvecs on the full H) and the
+// exp series.  Per-gamma cost O(n d^2) on top of one O(d^3) reduction, instead of G reductions.
+struct MgMem {
+  double2 *Y, *Z, *S, *Ku, *Qs, *Es, *gout;
+};
+
+template <int NW>
+struct MgShape {
+  // hb = full H (row stride HS = E0 + 1, at offset 1); u1 as Shape<NW> but with La Budde's q
+  // rows at stride QS = n + 2; then Y, Z [G][E0], S [G][n+1], Ku [NW][64], Qs [n+2],
+  // Es [NW][n+2], gout [G]
+  __host__ __device__ static int u1_words(int E0, int n) {
+    const int lab = (E0 + 1) * (n + 2) + 128 + 2 * NW;
+    return Shape<NW>::RED_END > lab ? Shape<NW>::RED_END : lab;
+  }
+  __host__ __device__ static int words(int E0, int G, int n) {
+    return 1 + E0 * (E0 + 1) + u1_words(E0, n) + 2 * G * E0 + G * (n + 1) + NW * 64 + (n + 2) +
+           NW * (n + 2) + G + 32 + 64 + 1;
+  }
+};
+
+template <int NW>
+__device__ __forceinline__ Mem carve_mg(double2 *b, int E0, int G, int n, MgMem &X) {
+  Mem M;
+  M.hb = b; b += 1 + E0 * (E0 + 1);
+  M.u1 = b; b += MgShape<NW>::u1_words(E0, n);
+  X.Y = b; b += G * E0;
+  X.Z = b; b += G * E0;
+  X.S = b; b += G * (n + 1);
+  X.Ku = b; b += NW * 64;
+  X.Qs = b; b += n + 2;
+  X.Es = b; b += NW * (n + 2);
+  X.gout = b; b += G;
+  M.wv = reinterpret_cast<int *>(b); b += 32;
+  M.ww = reinterpret_cast<double *>(b); b += 64;
+  M.beta = b;
+  return M;
+}
+
+template <int NW>
+__device__ __forceinline__ void team_tail_mg(const Pattern &D, int2 en, int E0, int G,
+                                             uint64_t zmask, const Mem &M, const MgMem &X,
+                                             int warp, int lane) {
+  const int n = D.n, E = en.x, NTL = en.y, HS = E0 + 1, BS = E0 + 2, QS = n + 2;
+  double2 *Q = M.u1;
+  double2 *Lr = Q + (E0 + 1) * QS;
+  if (NTL <= 32) labudde_levels_team<NW, 1, 32>(M.hb, Q, Lr, Lr + 128, E, NTL, BS, warp, lane, 0, QS, zmask);
+  else labudde_levels_team<NW, 1, 65>(M.hb, Q, Lr, Lr + 128, E, NTL, BS, warp, lane, 0, QS, zmask);
+  if (warp == 0) {  // c_M^{-1/2}, shared by every loop vector (c_M = q_0: no border here)
+    if (n + 2 <= 32) qhalf_coeffs<1>(Q, n, NTL, X.Qs, lane);
+    else qhalf_coeffs<2>(Q, n, NTL, X.Qs, lane);
+  }
+  const double2 *Hf = M.hb + 1;
+  double2 *u = X.Ku + warp * 64;
+  for (int g = warp; g < G; g += NW) {  // loop terms s_j = z'^T H^{j-1} y', j = 1..n
+    const double2 *y = X.Y + g * E0, *z = X.Z + g * E0;
+    const int i0 = lane, i1 = lane + 32;
+    const double2 z0 = i0 < E ? z[i0] : c0(), z1 = i1 < E ? z[i1] : c0();
+    double2 u0 = i0 < E ? y[i0] : c0(), u1v = i1 < E ? y[i1] : c0();
+    for (int j = 1; j <= n; ++j) {
+      const double2 sj = warp_sum2(cadd(cmul(z0, u0), cmul(z1, u1v)));
+      if (lane == 0) X.S[g * (n + 1) + j] = sj;
+      if (j == n) break;
+      u[i0] = u0;
+      u[i1] = u1v;
+      __syncwarp();
+      // (H u)_i = sub_i u_{i-1} + sum_{c >= i} H[i][c] u_c; unit subdiagonal except zero pivots
+      double2 a0 = c0(), a1 = c0();
+      if (i0 >= 1 && i0 < E && !((zmask >> i0) & 1ull)) a0 = u[i0 - 1];
+      if (i1 < E && !((zmask >> i1) & 1ull)) a1 = u[i1 - 1];
+      for (int c = 0; c < E; ++c) {
+        const double2 uc = u[c];
+        if (c >= i0 && i0 < E) a0 = cfma(Hf[i0 * HS + c], uc, a0);
+        if (c >= i1 && i1 < E) a1 = cfma(Hf[i1 * HS + c], uc, a1);
+      }
+      __syncwarp();
+      u0 = a0;
+      u1v = a1;
+    }
+  }
+  __syncthreads();  // Qs and every S written
+  for (int g = warp; g < G; g += NW) {
+    double2 gv;
+    if (n + 2 <= 32) gv = exp_dot<1>(X.Qs, X.S + g * (n + 1), n, X.Es + warp * (n + 2), lane);
+    else gv = exp_dot<2>(X.Qs, X.S + g * (n + 1), n, X.Es + warp * (n + 2), lane);
+    if (lane == 0) X.gout[g] = gv;
+  }
+  __syncthreads();
+}
+
+template <int NW, int C0, int C1, int C2, int C3, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB)
+sieve_mg_v5(JobDev J, uint64_t ubeg, uint64_t uend, int team_words) {
+  extern __shared__ double2 smem[];
+  __shared__ unsigned long long s_unit;
+  __shared__ double s_acc[LHAF_MAX_GAMMA][6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < team_words; i += 32 * NW) smem[i] = c0();
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_unit = ubeg + atomicAdd(J.counter, 1ull);
+    __syncthreads();
+    const uint64_t u = s_unit;
+    if (u >= uend) break;
+    const PatDesc P = J.descs[find_pattern(J, u)];
+    const Pattern D = pattern_of(P);
+    const int G = P.eta_b, E0 = D.E;
+    MgMem X;
+    const Mem M = carve_mg<NW>(smem, E0, G, D.n, X);
+    MgOut mg;
+    mg.Y = X.Y; mg.Z = X.Z; mg.YS = E0; mg.base = E0; mg.zmask = 0;
+    const uint64_t tb = (u - P.unit_begin) * P.chunk;
+    const uint64_t te = min(tb + P.chunk, P.T_eval);
+    if (threadIdx.x < G)
+      for (int q = 0; q < 6; ++q) s_acc[threadIdx.x][q] = 0.0;
+    for (uint64_t t = tb; t < te; ++t) {
+      int sign = 1;
+      double weight = 1.0;
+      const int2 en = team_reduce<NW, C0, C1, C2, C3, true>(P, D, J, t, M, warp, lane, sign, weight, &mg);
+      team_tail_mg<NW>(D, en, E0, G, mg.zmask, M, X, warp, lane);
+      // (sign and weight live in warp 0, lanes hold the same values)
+      const double sw = __shfl_sync(LHAF_FULL, sign * weight, 0), wt = __shfl_sync(LHAF_FULL, weight, 0);
+      if (warp == 0 && lane < G) {
+        const double2 gv = X.gout[lane];
+        dd_add(s_acc[lane][0], s_acc[lane][1], sw * gv.x);
+        dd_add(s_acc[lane][2], s_acc[lane][3], sw * gv.y);
+        dd_add(s_acc[lane][4], s_acc[lane][5], wt * hypot(gv.x, gv.y));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < G) {
+      const int g = threadIdx.x;
+      Partial q;
+      q.re_hi = s_acc[g][0]; q.re_lo = s_acc[g][1]; q.im_hi = s_acc[g][2]; q.im_lo = s_acc[g][3];
+      q.abs_hi = s_acc[g][4]; q.abs_lo = s_acc[g][5];
+      q.pad0 = 0; q.pad1 = 0;
+      J.partials[P.part_base + (uint64_t)g * P.units + (u - P.unit_begin)] = q;
+    }
   }
 }
 
@@ -577,6 +816,33 @@ cudaError_t launch_sieve_v5(const JobDev &job, int e_max, int ntl_max, int n_max
   if (e_max <= v5::I64::EMAX) LHAF_V5_CALL(I64, sieve)
 #undef sieve_ARGS
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sieve_mg_v5(const JobDev &job, int e_max, int g_max, int n_max, uint64_t ubeg,
+                               uint64_t uend, int num_sms, cudaStream_t s) {
+  if (uend <= ubeg) return cudaSuccess;
+  cudaError_t e = v5::ensure_inv();
+  if (e != cudaSuccess) return e;
+  if (e_max + g_max > 64 || g_max > LHAF_MAX_GAMMA) return cudaErrorInvalidValue;
+  constexpr int NW = 4;
+  const int tw = v5::MgShape<NW>::words(e_max, g_max, n_max);
+  const size_t smem = (size_t)tw * sizeof(double2);
+  // (the G loop-vector columns keep their positions through every compaction: the narrowest
+  // phase must still hold G + 1 columns, hence 3 positions per lane there, G <= 16)
+  auto *kern = v5::sieve_mg_v5<NW, 8, 6, 4, 3, 2>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NW, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  uint64_t grid = (uint64_t)num_sms * per_sm;
+  if (grid > uend - ubeg) grid = uend - ubeg;
+  e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, 32 * NW, smem, s>>>(job, ubeg, uend, tw);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_terms_v5(const JobDev &job, int e_max, int ntl_max, int n_max, const uint64_t *t,

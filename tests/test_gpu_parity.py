@@ -447,107 +447,58 @@ def test_cutoff_limits_single_mode_closed_form(lib):
 
 
 def test_multigamma_vs_oracle(lib, orc):
-    # SURVEY 8(f) row 2 (API level): one pattern, several loop vectors incl. gamma = 0
+    # one pattern, several loop vectors incl. gamma = 0 -- the shared cubic
+    # step (FLAG_MG: one reduction per term, loop vectors carried as inert rows/columns) against
+    # the oracle and against the separate evaluation of each loop vector
     rng = G.rng_for(388)
     k = 6
     A = G.random_symmetric(k, rng, 0.6)
     gs = np.stack([G.complex_gaussian(k, 0.5, rng) for _ in range(4)] + [np.zeros(k, complex)])
-    reps = [2, 1, 0, 1, 3, 1]
-    vals = lib.lhaf_rpt_multigamma(A, gs, reps)
-    assert vals.shape == (5,)
-    for g, v in zip(gs, vals):
-        assert rel(v, orc.lhaf(A, g, reps)) <= 1e-10
+    for reps in ([2, 1, 0, 1, 3, 1], [1, 1, 1, 1, 1, 0], [0, 3, 0, 2, 0, 0]):
+        vals = lib.lhaf_rpt_multigamma(A, gs, reps)
+        assert vals.shape == (5,)
+        os.environ["LHAF_MULTIGAMMA_SEPARATE"] = "1"
+        try:
+            sep = lib.lhaf_rpt_multigamma(A, gs, reps)
+        finally:
+            del os.environ["LHAF_MULTIGAMMA_SEPARATE"]
+        for g, v, w in zip(gs, vals, sep):
+            ref = orc.lhaf(A, g, reps)
+            if abs(ref) == 0.0:
+                assert abs(v) <= 1e-14
+                continue
+            assert rel(v, ref) <= 1e-10, (reps, v, ref)
+            assert rel(v, w) <= 1e-12, (reps, v, w)
 
 
-# ---------------------------------------------------------------- precise mode (lhaf_set_precision(1))
-@pytest.fixture
-def precise(lib):
-    lib.lhaf_set_precision(1)
+def test_multigamma_shared_full_width(lib, orc):
+    # d = 24 (a cfg2 pattern) with G = 16 loop vectors: d + G = 40 columns in the tile, every
+    # compaction phase; sampled against the oracle's ET
+    c2 = G.config(2)
+    rng = G.rng_for(389)
+    gs = np.stack([G.complex_gaussian(50, 0.2, rng) for _ in range(16)])
+    reps = c2["reps_batch"][0]
+    vals = lib.lhaf_rpt_multigamma(c2["A"], gs, reps)
+    for g in (0, 7, 15):
+        ref = orc.lhaf(c2["A"], gs[g], reps, method="et")
+        assert rel(vals[g], ref) <= 1e-10, (g, vals[g], ref)
+
+
+@pytest.mark.parametrize("reps", [[2, 2, 2, 1, 1], [4, 0, 2, 2, 1], [2, 2, 2, 2, 2]])
+def test_zero_weight_deletion_v5(lib, orc, reps):
+    # v5 removes zero-weight indices per term (w_h = 0 when eta_h = 2 k_h): terms of patterns
+    # with even repeats run at their own size; values against the oracle, with and without loops
+    rng = G.rng_for(390 + sum(reps))
+    k = len(reps)
+    A = G.pure_B(G.haar_unitary(k, rng), 0.8)
+    lib.lhaf_set_kernel(5)
     try:
-        yield lib
+        for g in (G.complex_gaussian(k, 0.4, rng), np.zeros(k, complex)):
+            ref = orc.lhaf(A, g, reps)
+            got = lib.lhaf_rpt(A, g, reps)
+            if abs(ref) == 0.0:
+                assert abs(got) <= 1e-14
+            else:
+                assert rel(got, ref) <= 1e-10, (reps, got, ref)
     finally:
-        lib.lhaf_set_precision(0)
-
-
-@pytest.mark.parametrize("seed", range(8))
-def test_precise_mode_small_vs_oracle(precise, orc, seed):
-    # the double-double tail on random small patterns: same values as the
-    # oracle's brute force / sieve, loops and no loops, odd N, collisions
-    lib = precise
-    rng = G.rng_for(700 + seed)
-    k = int(rng.integers(1, 9))
-    N = int(rng.integers(1, 17))
-    A = G.pure_B(G.haar_unitary(k, rng), 0.8) if seed % 2 else G.random_symmetric(k, rng)
-    g = np.zeros(k, complex) if seed % 4 == 0 else G.complex_gaussian(k, 0.5, rng)
-    reps = G.random_pattern(k, N, rng)
-    ref, T, sabs = orc.lhaf_fds(A, g, reps)
-    job = lib.Job(A, g, reps)
-    assert job.info.precision == 1 and job.info.kernel == 5
-    job.reset(); job.run(); got = job.finalize()[0]
-    job.close()
-    if abs(ref) < 1e-6 * sabs:
-        assert abs(got - ref) <= 1e-12 * sabs
-    else:
-        assert rel(got, ref) <= 1e-10, (reps, got, ref)
-
-
-@pytest.mark.parametrize("seed", range(4))
-def test_precise_mode_mixed_natural_vs_oracle(precise, orc, seed):
-    # precise mode plans mixed states by the natural pairing (reading C11)
-    lib = precise
-    rng = G.rng_for(720 + seed)
-    k = int(rng.integers(2, 6))
-    U = G.haar_unitary(k, rng)
-    A2 = G.lossy_squeezed_A2(U, 0.7, 0.5)
-    g2 = np.zeros(2 * k, complex) if seed % 2 else G.complex_gaussian(2 * k, 0.3, rng)
-    reps = G.random_pattern(k, int(rng.integers(1, 8)), rng)
-    info = lib.lhaf_plan(reps, mixed=1)
-    assert [q - p for p, q in info.pairs()] == [k] * info.H      # natural pairs (i, i + k)
-    ref = orc.lhaf_mixed(A2, g2, reps)
-    got = lib.lhaf_rpt_mixed(A2, g2, reps)
-    assert rel(got, ref) <= tol_for(2 * sum(reps)), (reps, got, ref)
-
-
-@pytest.mark.parametrize("which", ["cfg4_d60", "cfg5_d48_natural"])
-def test_per_term_parity_precise(precise, orc, which):
-    # P14 in precise mode: the per-term error falls to the FP64 Hessenberg's share (measured
-    # medians 9e-15 at cfg4 and 2.4e-15 at cfg5 with the natural pairing, vs 5e-14 and 1.4e-12 in
-    # FP64); asserted: max |err| / max |g| <= 1e-12 and median per-term error <= 3e-14
-    lib = precise
-    cfg = G.config(4 if which.startswith("cfg4") else 5)
-    mixed = cfg["mixed"]
-    C, v, eta, n = orc.reduced_system(cfg["A"], cfg["gamma"], cfg["reps"], mixed=mixed)
-    info = lib.lhaf_plan(cfg["reps"], mixed=mixed)
-    assert info.etas() == eta and info.n == n
-    job = lib.Job(cfg["A"], cfg["gamma"], cfg["reps"], mixed=mixed)
-    ts = G.rng_for(99).integers(0, info.T_eval, 512, dtype=np.uint64)
-    gg = job.terms_g(ts)
-    job.close()
-    W = np.array([orc.decode(int(t), eta)[1] for t in ts], np.int32)
-    refs = orc.fds_terms(C, v, W, n)
-    per_term = np.abs(gg - refs) / np.abs(refs)
-    scaled = np.abs(gg - refs).max() / np.abs(refs).max()
-    print(f"P14 precise {which}: per-term median {np.median(per_term):.2e} max {per_term.max():.2e}; "
-          f"max |err| / max |g| {scaled:.2e}")
-    assert scaled <= 1e-12 and np.median(per_term) <= 3e-14, (which, scaled, np.median(per_term))
-
-
-def test_cutoff_error_estimates(lib, orc):
-    # lhaf_rpt_cutoff_ex: the per-count estimate kappa_j 2^-46 bounds the observed error against
-    # the oracle at every count, grows with the batched count, and tol refuses counts past it
-    rng = G.rng_for(5240)
-    k = 6
-    A = G.pure_B(G.haar_unitary(k, rng), 0.7)
-    g = G.complex_gaussian(k, 0.3, rng)
-    fixed = np.array([1, 1, 0, 1, 0, 1], np.int32)
-    vals, err = lib.lhaf_rpt_cutoff_ex(A, g, fixed, 2, 12)
-    assert np.allclose(vals, lib.lhaf_rpt_cutoff(A, g, fixed, 2, 12), rtol=0, atol=0)
-    for c in range(13):
-        reps = fixed.copy()
-        reps[2] = c
-        ref = orc.lhaf(A, g, reps)
-        assert rel(vals[c], ref) <= max(err[c], 1e-15), (c, rel(vals[c], ref), err[c])
-    assert err[12] > err[0]
-    with pytest.raises(lib.LhafError) as e:
-        lib.lhaf_rpt_cutoff_ex(A, g, fixed, 2, 12, tol=err[6] * 0.5)
-    assert e.value.status == 7
+        lib.lhaf_set_kernel(0)
