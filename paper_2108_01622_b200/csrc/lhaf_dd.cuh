@@ -5,7 +5,7 @@
 // Why these two stages: the per-term rounding error of the FP64 pipeline at the BASELINE sizes
 // is dominated by La Budde (the coefficient recursion cancels) and, for the natural pairing of
 // mixed states, by the series; the Hessenberg reduction itself contributes ~1e-15..1e-14
-// (tools/proto/stage_errors.py: each stage swapped to long double in turn).  Carrying the
+// (tests/diag/stage_errors.py: each stage swapped to long double in turn).  Carrying the
 // characteristic-polynomial coefficients and the series in double-double leaves the FP64
 // reduction as the only per-term error source.
 #pragma once

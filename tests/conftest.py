@@ -27,3 +27,6 @@ def lib():
     b.build()
     import paper_2108_01622_b200 as L
     return L
+
+# tests/diag holds oracle-comparison scripts run by hand, not pytest modules
+collect_ignore_glob = ["diag/*"]

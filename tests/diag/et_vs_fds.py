@@ -4,7 +4,7 @@ finite-difference sieve (lhaf_rpt, FP64; and in precise mode up to --precise-max
 inclusion/exclusion (lhaf_rpt_et: the v5 kernel deletes each term's excluded pairs, so a term
 is reduced at its own size -- P:445), with the reference product from the CPU oracle in x87 long
 double (ET tier at N/2).  Device-synchronous wall time per call.  One JSON line per N.
-    python tools/et_vs_fds.py [N ...] [--inst=K] [--precise-max=N]"""
+    python tests/diag/et_vs_fds.py [N ...] [--inst=K] [--precise-max=N]"""
 import json
 import os
 import sys
@@ -12,7 +12,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import gbs_inputs as G  # noqa: E402
 import oracle  # noqa: E402  (reference values only)

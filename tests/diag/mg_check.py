@@ -1,7 +1,7 @@
 """GPU check of the gamma-batched evaluation (FLAG_MG) and of zero-weight deletion (ET):
 values vs the oracle and the separate evaluation, and the cost of G loop vectors against one."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import gbs_inputs as G
 import oracle as O

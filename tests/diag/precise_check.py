@@ -1,7 +1,7 @@
 """GPU check of the precise mode (double-double La Budde + series): per-term errors vs the
 long-double oracle (fast vs precise), block-diagonal sums, and the cost on cfg slices."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import gbs_inputs as G
 import oracle as O

@@ -5,7 +5,7 @@ fp64 vs the long-double oracle term, on config-4-like matrices.  Pipelines:
   S: complex-symmetric tridiagonalisation with complex-orthogonal reflectors
 all followed by trailing La Budde + first-row loop correction + det^{-1/2} / exp series."""
 import sys, numpy as np
-sys.path.insert(0, '/root/repo')
+import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle as O, gbs_inputs as G
 
 def series_g(c, Dt, beta, n, d):

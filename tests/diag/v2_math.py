@@ -7,7 +7,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, '/root/repo')
+import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import gbs_inputs as G  # noqa: E402
 import oracle as O  # noqa: E402
 

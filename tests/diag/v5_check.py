@@ -1,7 +1,7 @@
 """Quick GPU check of a kernel variant against v3 and the oracle, and a timing of a cfg slice.
-python tools/v5_check.py [variant=5]"""
+python tests/diag/v5_check.py [variant=5]"""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import gbs_inputs as G
 import oracle as O
