@@ -253,6 +253,7 @@ int lhaf::set_error(int status, const char *msg) {
 // ------------------------------------------------------------------ job
 struct lhaf_job {
   int batch = 0, kdim = 0, d_max = 0, n_max = 0, variant = 1, prec = 0;
+  int scale_s = 0;  // exact input scaling 2^s per photon (results multiplied back by 2^{-sN})
   int e_max = 0, ntl_max = 0;   // bordered dimension E and leading coefficients NTL
   bool any_loop = false;
   uint64_t units = 0, terms = 0, plan_bytes = 0;
@@ -340,9 +341,38 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     ghost = gcopy.data();
   }
 
+  // Exact power-of-two input scaling: lhaf(4^s A, 2^s gamma) = 2^{sN} lhaf(A, gamma)
+  // (each photon contributes one factor 2^s: a pair one A entry, a loop one gamma entry; the
+  // phantom's loop 1 is unscaled and is always a loop).  Inputs far from unit scale are brought
+  // to ~1 before upload, so that no pivot, characteristic-polynomial coefficient or series term
+  // under- or overflows; the finalize multiplies by 2^{-sN}.  Host inputs only (device buffers
+  // belong to the caller); |s| < 8 leaves the inputs untouched.
+  int scale_s = 0;
+  std::vector<double> a_scaled, g_scaled;
+  if (!on_device) {
+    double ma = 0.0, mg = 0.0;
+    for (size_t i = 0; i < (size_t)kdim * kdim; ++i) ma = std::max(ma, std::hypot(A[2 * i], A[2 * i + 1]));
+    for (size_t i = 0; i < gamma_len; ++i) mg = std::max(mg, std::hypot(ghost[2 * i], ghost[2 * i + 1]));
+    const double m = std::max(std::sqrt(ma), mg);
+    if (m > 0.0 && std::isfinite(m)) {
+      const int s0 = -(int)std::lround(std::log2(m));
+      if (std::abs(s0) >= 8 && std::abs(s0) <= 400) scale_s = s0;
+    }
+    if (scale_s != 0) {
+      a_scaled.assign(A, A + 2 * (size_t)kdim * kdim);
+      for (double &x : a_scaled) x = std::ldexp(x, 2 * scale_s);
+      g_scaled.assign(ghost, ghost + 2 * gamma_len);
+      for (double &x : g_scaled) x = std::ldexp(x, scale_s);
+      A = a_scaled.data();
+      gamma = g_scaled.data();
+      ghost = g_scaled.data();
+    }
+  }
+
   lhaf_job *j = new lhaf_job();
   j->batch = batch;
   j->kdim = kdim;
+  j->scale_s = scale_s;
   j->variant = 1;
   std::vector<int32_t> ipool;
   std::vector<double> dpool;
@@ -401,6 +431,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       }
     }
     D.T_eval = P.T_eval;
+    D.out_exp = -scale_s * P.N;  // the photons of this pattern (for mixed: of the 2N x 2N matrix)
     D.gamma_off = gamma_stride ? (int64_t)b * gamma_stride : 0;
     D.unit_begin = unit;
     D.part_base = (int64_t)part;
@@ -859,6 +890,7 @@ static lhaf_status cutoff_impl(const double *A, const double *gamma, const int32
     D.n = n_f[c & 1] + m;
     D.unit_begin = (uint64_t)G.part_base + (uint64_t)m * G.units;
     D.units = G.units;
+    D.out_exp = -j->scale_s * (Pf.N + c);
   }
   PatDesc *d_vd = nullptr;
   double2 *d_o = nullptr;
@@ -916,6 +948,7 @@ lhaf_status lhaf_rpt_multigamma(const double *A, const double *gammas, int32_t n
     vd[g].n = D.n;
     vd[g].unit_begin = (uint64_t)D.part_base + (uint64_t)g * D.units;
     vd[g].units = D.units;
+    vd[g].out_exp = D.out_exp;
   }
   PatDesc *d_vd = nullptr;
   double2 *d_o = nullptr;

@@ -26,7 +26,7 @@ struct PatDesc {
   // j in [0, 2 eta_b] gives w = j - eta_b; outputs m = 0..eta_b (count 2m + parity) go to
   // partials[part_base + m * units + unit - unit_begin]
   int32_t eta_b;
-  int32_t pad_;
+  int32_t out_exp;     // extra power-of-two exponent of the result (input scaling, see lhaf_host.cpp)
   int64_t part_base;
 };
 

@@ -502,3 +502,23 @@ def test_zero_weight_deletion_v5(lib, orc, reps):
                 assert rel(got, ref) <= 1e-10, (reps, got, ref)
     finally:
         lib.lhaf_set_kernel(0)
+
+
+@pytest.mark.parametrize("e", [-100, -40, 60])
+def test_extreme_input_scales(lib, orc, e):
+    # homogeneity lhaf(4^e A, 2^e gamma) = 2^{eN} lhaf(A, gamma) at scales where the raw
+    # characteristic-polynomial coefficients (~4^{e t}) or the pivots (~4^e) would leave the
+    # double range: the library normalises host inputs by an exact power of two and restores the
+    # scale in the finalize, so the result is the unscaled one times 2^{eN} exactly
+    rng = G.rng_for(7100)
+    k = 6
+    A = G.pure_B(G.haar_unitary(k, rng), 0.8)
+    g = G.complex_gaussian(k, 0.4, rng)
+    for reps in ([2, 1, 1, 0, 1, 1], [1, 1, 1, 1, 1, 1], [3, 0, 1, 2, 0, 0]):
+        N = sum(reps)
+        base = lib.lhaf_rpt(A, g, reps)
+        got = lib.lhaf_rpt(np.ldexp(A.real, 2 * e) + 1j * np.ldexp(A.imag, 2 * e),
+                           np.ldexp(g.real, e) + 1j * np.ldexp(g.imag, e), reps)
+        want = complex(np.ldexp(base.real, e * N), np.ldexp(base.imag, e * N))
+        assert got == want, (e, reps, got, want)
+        assert rel(base, orc.lhaf(A, g, reps)) <= 1e-10
