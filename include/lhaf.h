@@ -136,7 +136,9 @@ lhaf_status lhaf_rpt_cutoff(const double *A, const double *gamma, const int32_t 
  * is the FP64 per-term relative error scale measured for d <= 48).  The
  * repeated-pair sieve cancels steeply with the count of one mode (tanh r = 0.6: kappa*eps ~ 2e-8,
  * 8e-5, 1e-2, 1 at counts 4, 8, 12, 16 -- profiles/r01/cutoff_kappa_t0.6.txt), so high counts
- * of a strongly squeezed mode are beyond FP64.  tol > 0: if some err_est[j] > tol, out and
+ * of a strongly squeezed mode are beyond FP64.  err_est is capped at 1 (a value at the noise
+ * level of its own terms, e.g. an exact zero, has no significant digits).  tol > 0: if some
+ * err_est[j] > tol, out and
  * err_est are still written and LHAF_E_INACCURATE is returned (lhaf_last_error names the first
  * such count); tol <= 0 never refuses.  err_est: n_cut + 1 doubles.  Other errors as
  * lhaf_rpt_cutoff. */

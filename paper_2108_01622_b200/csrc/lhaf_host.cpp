@@ -795,14 +795,15 @@ lhaf_status lhaf_rpt_cutoff_ex(const double *A, const double *gamma, const int32
   int worst = -1;
   for (int c = 0; c <= n_cut; ++c) {
     const double v = std::hypot(out[2 * c], out[2 * c + 1]);
-    // kappa = 2^{1-n} sum |term| / |lhaf| times the per-term error scale 2^-46 (~64 eps)
-    const double kap = v > 0.0 ? ab[c] / v : (ab[c] > 0.0 ? INFINITY : 1.0);
-    err_est[c] = kap * 0x1p-46;
+    // kappa = 2^{1-n} sum |term| / |lhaf| times the per-term error scale 2^-46 (~64 eps), capped
+    // at 1 (a value at the rounding-noise level of its terms -- e.g. an exact zero -- has no
+    // significant digits)
+    err_est[c] = ab[c] > 0.0 ? std::min(1.0, ab[c] * 0x1p-46 / std::max(v, 1e-300)) : 0.0;
     if (tol > 0.0 && err_est[c] > tol && worst < 0) worst = c;
   }
   if (worst >= 0)
-    return fail(LHAF_E_INACCURATE, "count %d: estimated relative error %.2e > tol %.2e (sieve cancellation kappa %.2e)",
-                worst, err_est[worst], tol, err_est[worst] / 0x1p-46);
+    return fail(LHAF_E_INACCURATE, "count %d: estimated relative error %.2e > tol %.2e (sieve cancellation)",
+                worst, err_est[worst], tol);
   return LHAF_OK;
 }
 
