@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblhaf.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("lhaf_kernels.cu", "lhaf_v3.cu", "lhaf_v5.cu", "lhaf_host.cpp", "lhaf_gbs.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("lhaf_kernels.cu", "lhaf_v3.cu", "lhaf_v5.cu", "lhaf_tree.cu", "lhaf_host.cpp", "lhaf_gbs.cpp")]
 HEADERS = [os.path.join(CSRC, "lhaf_internal.h"), os.path.join(CSRC, "lhaf_device.cuh"), os.path.join(CSRC, "lhaf_tail.cuh"), os.path.join(ROOT, "include", "lhaf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -209,6 +209,30 @@ lhaf_status check_plan_limits(const Plan &P) {
   return LHAF_OK;
 }
 
+// Tree order of the pairs (variant 6): the pair eliminated first (tree index H-1, depth 0) has
+// an odd eta -- the smallest odd one -- so that halving (reading C6) keeps the first (eta+1)/2
+// digits of the root; the others follow by descending eta, so that the pairs with the most
+// digits are eliminated last, where the matrices are smallest.  Any order gives the same lhaf
+// (every matching does; the sieve sum does not depend on the order of its pairs).
+// Returns false (no halving) when every eta is even.
+bool tree_order(Plan &P) {
+  const int H = P.H;
+  std::vector<int> idx(H);
+  for (int h = 0; h < H; ++h) idx[h] = h;
+  int root = -1;
+  for (int h = 0; h < H; ++h)
+    if ((P.eta[h] & 1) && (root < 0 || P.eta[h] < P.eta[root])) root = h;
+  std::vector<int> rest;
+  for (int h = 0; h < H; ++h)
+    if (h != root) rest.push_back(h);
+  std::stable_sort(rest.begin(), rest.end(), [&](int a, int b) { return P.eta[a] > P.eta[b]; });
+  if (root >= 0) rest.push_back(root);
+  std::vector<int> p(H), q(H), eta(H);
+  for (int t = 0; t < H; ++t) { p[t] = P.p[rest[t]]; q[t] = P.q[rest[t]]; eta[t] = P.eta[rest[t]]; }
+  P.p = p; P.q = q; P.eta = eta;
+  return root >= 0;
+}
+
 lhaf_status check_symmetric(const double *A, int m) {
   double amax = 0.0, dmax = 0.0;
   for (int i = 0; i < m; ++i)
@@ -271,6 +295,10 @@ struct lhaf_job {
   unsigned long long *d_counter = nullptr;
   double2 *d_out = nullptr;
   double *d_abs = nullptr;
+  // variant 6: one tree per group of patterns of the same shape
+  std::vector<TreeGroup> groups;
+  TreeWork tw;
+  double tree_flops = 0.0;
   JobDev dev() const {
     JobDev J;
     J.descs = d_descs; J.npat = batch; J.ipool = d_ipool; J.dpool = d_dpool; J.upool = d_upool;
@@ -287,6 +315,8 @@ static void job_free(lhaf_job *j) {
   dfree(j->d_cpool);
   if (j->own_inputs) { dfree(j->d_A); dfree(j->d_gamma); }
   dfree(j->d_partials); dfree(j->d_counter); dfree(j->d_out); dfree(j->d_abs);
+  for (auto &g : j->groups) dfree(g.d_pats);
+  tree_work_free(j->tw);
   delete j;
 }
 
@@ -369,6 +399,13 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     }
   }
 
+  // variant 6 (the prefix-sharing tree) evaluates plain sieves: not the cutoff groups, the
+  // inclusion/exclusion terms or the gamma-batched jobs (their own kernels), not precise mode
+  bool use_tree = g_ctx.variant == 6 || (g_ctx.variant == 0 && g_ctx.precision == 0);
+  if (plans_in)
+    for (const Plan &Pm : *plans_in)
+      if (Pm.et || Pm.eta_b >= 0 || Pm.mg > 0) use_tree = false;
+
   lhaf_job *j = new lhaf_job();
   j->batch = batch;
   j->kdim = kdim;
@@ -401,11 +438,16 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     } else {
       s = make_plan(reps + (size_t)b * k, k, mixed, P);
     }
+    bool full = false;
+    if (s == LHAF_OK && use_tree && P.H > 0 && !tree_order(P)) {
+      full = true;       // every eta even: no halving, the whole range [0, T)
+      P.T_eval = P.T;
+    }
     if (s == LHAF_OK) s = check_plan_limits(P);
     if (s != LHAF_OK) { job_free(j); return s; }
     PatDesc &D = j->descs[b];
     memset(&D, 0, sizeof D);
-    D.d = P.d; D.H = P.H; D.n = P.n; D.flags = 0;
+    D.d = P.d; D.H = P.H; D.n = P.n; D.flags = full ? FLAG_FULL : 0;
     if (P.mg > 0) {
       // gamma-batched: M alone is reduced (no border); the loop vectors ride along (v5 MG)
       D.flags |= FLAG_MG;
@@ -443,9 +485,9 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       D.chunk = std::max<uint64_t>(64, (P.T_eval + 4095) / 4096);
       if (D.chunk > P.T_eval) D.chunk = P.T_eval;
     } else {
-      D.chunk = chunk_for(P.T_eval, small_job);
+      D.chunk = use_tree ? 0 : chunk_for(P.T_eval, small_job);
     }
-    D.units = (P.T_eval + D.chunk - 1) / D.chunk;
+    D.units = use_tree ? 0 : (P.T_eval + D.chunk - 1) / D.chunk;  // tree jobs: units below
     unit += D.units;
     part += D.units * (uint64_t)(P.mg > 0 ? P.mg : P.eta_b >= 0 ? P.eta_b + 1 : 1);
     j->terms += P.T_eval;
@@ -473,6 +515,41 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     D.mat_off = cpool_words;
     cpool_words += (int64_t)(P.d + 1) * (P.d + 1) + 2 * P.d + 2;  // v1: Ct|uh|v|beta; v3/v5: E x E
   }
+  if (use_tree) {
+    // groups of patterns with the same tree shape; each group's units are contiguous
+    std::vector<std::vector<int>> keys;
+    for (int b = 0; b < batch; ++b) {
+      const PatDesc &D = j->descs[b];
+      if (D.H == 0 || D.T_eval == 0) continue;
+      std::vector<int> key = {D.H, D.n, (D.flags & FLAG_LOOP) ? 1 : 0, (D.flags & FLAG_FULL) ? 0 : 1};
+      for (int h = 0; h < D.H; ++h) key.push_back(ipool[D.eta_off + h]);
+      size_t gi = 0;
+      while (gi < keys.size() && keys[gi] != key) ++gi;
+      if (gi == keys.size()) {
+        keys.push_back(key);
+        TreeGroup g;
+        g.H = D.H; g.n = D.n; g.bord = key[2]; g.halve = key[3];
+        g.eta.assign(key.begin() + 4, key.end());
+        j->groups.push_back(g);
+      }
+      j->groups[gi].pats.push_back(b);
+    }
+    for (auto &g : j->groups) {
+      g.npat = (int)g.pats.size();
+      tree_plan_group(g, 8192);
+      g.unit_base = unit;
+      for (int32_t pb : g.pats) {
+        PatDesc &D = j->descs[pb];
+        D.unit_begin = unit;
+        D.units = g.units_pp;
+        D.chunk = D.T_eval / g.units_pp;  // leaves per unit
+        D.part_base = (int64_t)unit;
+        unit += g.units_pp;
+      }
+      part = unit;
+      j->tree_flops = 8.0 * tree_cmacs_per_term(g);
+    }
+  }
   j->units = unit;
   j->parts = part;
   j->plan_bytes = j->descs.size() * sizeof(PatDesc) + ipool.size() * 4 + dpool.size() * 8 +
@@ -486,6 +563,8 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   if (e == cudaSuccess) e = dmalloc(&j->d_partials, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
   if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
   if (e == cudaSuccess) e = dmalloc(&j->d_counter, sizeof(unsigned long long));
+  for (auto &g : j->groups)
+    if (e == cudaSuccess) e = upload(&g.d_pats, g.pats);
   if (e == cudaSuccess) e = dmalloc(&j->d_out, std::max(1, batch) * sizeof(double2));
   if (e == cudaSuccess) e = dmalloc(&j->d_abs, std::max(1, batch) * sizeof(double));
   if (on_device) {
@@ -500,21 +579,23 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     if (e == cudaSuccess && gamma_len > 0)
       e = cudaMemcpy(j->d_gamma, gamma, gamma_len * sizeof(double2), cudaMemcpyHostToDevice);
   }
-  j->variant = g_ctx.variant ? g_ctx.variant : choose_variant(j->e_max, j->n_max);
+  j->variant = use_tree ? 6 : g_ctx.variant ? g_ctx.variant : choose_variant(j->e_max, j->n_max);
   j->prec = g_ctx.precision;
-  if (j->prec) j->variant = 5;  // the precise tail lives in the v5 kernel (every E <= 64)
+  if (j->prec && !use_tree) j->variant = 5;  // the precise tail lives in the v5 kernel (every E <= 64)
   // inclusion/exclusion: excluded pairs are zero columns -- v5 deletes them per term (reduction
   // at the term's own size), which is where ET's cost advantage comes from
   bool any_et = false;
   for (const auto &D : j->descs) any_et = any_et || (D.flags & FLAG_ET);
   if (any_et && g_ctx.variant == 0 && v5_supported(j->e_max)) j->variant = 5;
   if (j->variant == 0 || (j->variant == 5 && !v5_supported(j->e_max))) j->variant = 3;
-  if (j->prec && j->variant != 5) {
+  if (j->prec && j->variant != 5 && j->variant != 6) {
     job_free(j);
     return fail(LHAF_E_TOO_LARGE, "precise mode needs d <= 63 (bordered size <= 64)");
   }
-  if (j->variant >= 3 && !bordered_supported(j->e_max, j->n_max)) j->variant = 1;
-  if (e == cudaSuccess) e = (j->variant >= 3) ? launch_prep_bordered(j->dev(), 0) : launch_prep(j->dev(), j->d_max, 0);
+  if (j->variant >= 3 && j->variant != 6 && !bordered_supported(j->e_max, j->n_max)) j->variant = 1;
+  // tree jobs build their roots per run; the bordered B0 serves lhaf_job_terms (v3 per term)
+  if (e == cudaSuccess && !(j->variant == 6 && !bordered_supported(j->e_max, j->n_max)))
+    e = (j->variant >= 3) ? launch_prep_bordered(j->dev(), 0) : launch_prep(j->dev(), j->d_max, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     job_free(j);
@@ -525,6 +606,17 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
 }
 
 static cudaError_t run_sieve(lhaf_job *j, uint64_t b, uint64_t e, cudaStream_t st) {
+  if (j->variant == 6) {
+    for (auto &g : j->groups) {
+      const uint64_t gb = g.unit_base, ge = gb + (uint64_t)g.npat * g.units_pp;
+      const uint64_t lo = std::max(b, gb), hi = std::min(e, ge);
+      if (lo < hi) {
+        cudaError_t r = tree_run(j->dev(), g, j->tw, lo - gb, hi - gb, st);
+        if (r != cudaSuccess) return r;
+      }
+    }
+    return cudaSuccess;
+  }
   if (j->variant == 5)
     return launch_sieve_v5(j->dev(), j->e_max, j->ntl_max, j->n_max, b, e, g_ctx.num_sms, st, j->prec);
   if (j->variant == 3)
@@ -630,8 +722,8 @@ lhaf_status lhaf_set_precision(int32_t mode) {
 int32_t lhaf_get_precision(void) { return g_ctx.precision; }
 
 lhaf_status lhaf_set_kernel(int32_t variant) {
-  if (variant != 0 && variant != 1 && variant != 3 && variant != 5)
-    return fail(LHAF_E_ARG, "unknown kernel variant %d (0 = default, 1 = Householder, 3 = v3, 5 = v5)", variant);
+  if (variant != 0 && variant != 1 && variant != 3 && variant != 5 && variant != 6)
+    return fail(LHAF_E_ARG, "unknown kernel variant %d (0 = default, 1 = Householder, 3 = v3, 5 = v5, 6 = tree)", variant);
   g_ctx.variant = variant;
   return LHAF_OK;
 }
@@ -653,7 +745,8 @@ lhaf_status lhaf_job_info_get(const lhaf_job *j, lhaf_job_info *info) {
   for (const auto &D : j->descs)
     if (D.d > 0) {
       const bool lp = (D.flags & FLAG_LOOP) != 0;
-      info->flops_per_term_model = (j->variant >= 3)   ? v3_flops_per_term(D.d, D.n, lp)
+      info->flops_per_term_model = (j->variant == 6)  ? j->tree_flops
+                                   : (j->variant >= 3) ? v3_flops_per_term(D.d, D.n, lp)
                                                        : flops_per_term(j->variant, D.d, D.n, true);
       break;
     }
@@ -746,7 +839,7 @@ lhaf_status lhaf_job_terms(lhaf_job *j, const uint64_t *t, int32_t nt, double *g
   if (e == cudaSuccess) {
     const PatDesc &D0 = j->descs[0];
     e = (j->variant == 5)   ? launch_terms_v5(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0, j->prec)
-        : (j->variant == 3) ? launch_terms_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
+        : (j->variant == 3 || j->variant == 6) ? launch_terms_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, dt, nt, dg, 0)
                             : launch_terms(j->dev(), j->variant, D0.d, D0.n, dt, nt, dg, 0);
   }
   if (e == cudaSuccess) e = cudaMemcpy(g_out, dg, nt * sizeof(double2), cudaMemcpyDeviceToHost);

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace lhaf {
 
 // One pattern of a job.  All offsets index the job's device pools.
@@ -40,6 +42,9 @@ constexpr uint32_t FLAG_ET = 4u;
 // part_base + g * units + unit - unit_begin
 constexpr uint32_t FLAG_MG = 8u;
 constexpr int LHAF_MAX_GAMMA = 16;
+// FLAG_FULL: no halving (every eta even, so no pair has an odd digit count): the whole term
+// range is evaluated and the prefactor is 2^{-n} instead of 2^{1-n} (variant 6)
+constexpr uint32_t FLAG_FULL = 16u;
 
 // Chunk partial: double-double complex sum of the unit's terms + sum |term|.
 struct Partial {
@@ -100,6 +105,37 @@ cudaError_t launch_sieve_v5(const JobDev &job, int e_max, int ntl_max, int n_max
                             uint64_t unit_end, int num_sms, cudaStream_t s, int prec);
 cudaError_t launch_terms_v5(const JobDev &job, int e_max, int ntl_max, int n_max, const uint64_t *t,
                             int nt, double2 *g_out, cudaStream_t s, int prec);
+
+// Variant 6 (lhaf_tree.cu): the sieve terms of a pattern as the leaves of a tree that shares
+// every prefix of eliminated pairs (symmetric 2x2-block Schur complements of power series).
+namespace tree {
+struct TLevel {   // the nodes of one depth: K[(s * NE + e) * cap + node], logc[s * cap + node]
+  double2 *K;
+  double2 *logc;
+  double *coef;   // sign * prod C(eta, k) of the node's path
+  uint64_t cap;
+};
+}  // namespace tree
+struct TreeGroup {            // patterns that share one tree shape
+  int H = 0, n = 0, bord = 0, halve = 1, k_u = 0, npat = 0;
+  std::vector<int> eta;       // tree order: pair H-1 is eliminated first (depth 0)
+  std::vector<int32_t> pats;  // job pattern indices, in unit order
+  int32_t *d_pats = nullptr;
+  uint64_t unit_base = 0;     // first job unit of the group
+  uint64_t units_pp = 0;      // units per pattern = nodes at depth k_u
+};
+struct TreeWork {             // device buffers of the tree driver, kept across calls
+  static constexpr size_t kLevelBudget = (size_t)192 << 20;  // bytes per depth
+  std::vector<tree::TLevel> lv;
+  std::vector<size_t> kbytes, lbytes, cbytes;
+  void *scratch = nullptr, *val = nullptr, *absv = nullptr;
+  size_t scratch_bytes = 0, val_bytes = 0, abs_bytes = 0;
+};
+void tree_plan_group(TreeGroup &g, uint64_t target_units);
+double tree_cmacs_per_term(const TreeGroup &g);
+// group-local units [ub, ue) of group g (their partials at g.unit_base + u)
+cudaError_t tree_run(const JobDev &J, TreeGroup &g, TreeWork &w, uint64_t ub, uint64_t ue, cudaStream_t st);
+void tree_work_free(TreeWork &w);
 
 // sets lhaf_last_error() for entry points outside lhaf_host.cpp (returns its status argument)
 int set_error(int status, const char *msg);

@@ -412,8 +412,9 @@ __global__ void __launch_bounds__(128) finalize_kernel(JobDev J, double2 *out, d
     dd_add_dd(a2, a3, s[i][2], s[i][3]);
     dd_add_dd(a4, a5, s[i][4], s[i][5]);
   }
-  // 2^{1-n}: halving (x2) and the 2^{-n} prefactor, exact; 1 for inclusion/exclusion
-  const int e = ((P.flags & FLAG_ET) ? 0 : 1 - P.n) + P.out_exp;
+  // 2^{1-n}: halving (x2) and the 2^{-n} prefactor, exact; 2^{-n} without halving (FLAG_FULL);
+  // 1 for inclusion/exclusion
+  const int e = ((P.flags & FLAG_ET) ? 0 : (P.flags & FLAG_FULL) ? -P.n : 1 - P.n) + P.out_exp;
   out[p] = make_double2(ldexp(a0 + a1, e), ldexp(a2 + a3, e));
   if (abs_out) abs_out[p] = ldexp(a4 + a5, e);
 }

@@ -1,0 +1,138 @@
+"""GPU parity of kernel variant 6 (the prefix-sharing tree) against the oracle,
+and its work-unit invariants.
+
+The tree evaluates the same sieve terms as the per-term kernels but shares the
+Schur complements of every eliminated prefix of pairs; these tests pin it to the oracle on
+the shapes where its code paths differ: collisions (several digits per level, zero weights =
+deleted pairs), all-even multiplicities (no halving, FLAG_FULL), a single pair (the root is the
+leaf level), odd N (phantom), loops on and off (border index), mixed states, batches whose
+patterns fall into several tree shapes, and unit ranges (bit-identical results for any slicing).
+Tolerances: the north_star's 1e-10 for N <= 24 (relative), absolute against sum|term| where the
+exact value is 0 (reading C18).
+"""
+import numpy as np
+import pytest
+
+import gbs_inputs as G
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+@pytest.fixture()
+def tree(lib):
+    lib.lhaf_set_kernel(6)
+    yield lib
+    lib.lhaf_set_kernel(0)
+
+
+def check(got, ref, sabs, tol=1e-10):
+    if abs(ref) < 1e-6 * sabs:
+        assert abs(got - ref) <= 1e-12 * sabs, (got, ref, sabs)
+    else:
+        assert rel(got, ref) <= tol, (got, ref)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_tree_random_collisions(tree, orc, seed):
+    rng = G.rng_for(7000 + seed)
+    k = int(rng.integers(1, 8))
+    N = int(rng.integers(1, 21))
+    A = G.pure_B(G.haar_unitary(k, rng), 0.8) if seed % 2 else G.random_symmetric(k, rng)
+    g = np.zeros(k, complex) if seed % 3 == 0 else G.complex_gaussian(k, 0.5, rng)
+    reps = G.random_pattern(k, N, rng)
+    ref, T, sabs = orc.lhaf_fds(A, g, reps)
+    got = tree.lhaf_rpt(A, g, reps)
+    check(got, ref, sabs)
+
+
+@pytest.mark.parametrize("reps", [[1], [2], [3], [4], [6], [2, 2], [4, 2], [2, 2, 2], [1, 1], [5, 1]])
+def test_tree_single_and_even(tree, orc, reps):
+    # one pair (the root is the leaf level), self-pairs, and all-even multiplicities (every eta
+    # even after matching: no halving, the whole range is evaluated, prefactor 2^-n)
+    rng = G.rng_for(7100 + sum(reps) * 10 + len(reps))
+    k = len(reps)
+    A = G.random_symmetric(k, rng, 0.7)
+    g = G.complex_gaussian(k, 0.6, rng)
+    ref, T, sabs = orc.lhaf_fds(A, g, reps)
+    check(tree.lhaf_rpt(A, g, reps), ref, sabs)
+    ref0, _, sabs0 = orc.lhaf_fds(A, np.zeros(k, complex), reps)
+    check(tree.lhaf_rpt(A, np.zeros(k, complex), reps), ref0, sabs0)
+
+
+def test_tree_vs_v3_cfg1_cfg3(lib, orc):
+    for cfgn in (1, 3):
+        cfg = G.config(cfgn)
+        lib.lhaf_set_kernel(6)
+        t = lib.lhaf_rpt(cfg["A"], cfg["gamma"], cfg["reps"])
+        lib.lhaf_set_kernel(3)
+        v = lib.lhaf_rpt(cfg["A"], cfg["gamma"], cfg["reps"])
+        lib.lhaf_set_kernel(0)
+        ref, T, sabs = orc.lhaf_fds(cfg["A"], cfg["gamma"], cfg["reps"])
+        check(t, ref, sabs, 1e-10 if cfgn == 1 else 1e-8)
+        assert abs(t - v) <= 1e-8 * max(abs(ref), 1e-12 * sabs)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tree_mixed(tree, orc, seed):
+    rng = G.rng_for(7200 + seed)
+    k = int(rng.integers(2, 6))
+    A2 = G.lossy_squeezed_A2(G.haar_unitary(k, rng), 0.7, 0.5)
+    g2 = np.zeros(2 * k, complex) if seed % 2 else G.complex_gaussian(2 * k, 0.3, rng)
+    reps = G.random_pattern(k, int(rng.integers(1, 8)), rng)
+    ref = orc.lhaf_mixed(A2, g2, reps)
+    assert rel(tree.lhaf_rpt_mixed(A2, g2, reps), ref) <= 1e-10
+
+
+def test_tree_batch_shapes(tree, orc):
+    # a batch whose patterns fall into several tree shapes (different H, n, eta, loop flags):
+    # each shape is its own group with contiguous units
+    rng = G.rng_for(7300)
+    k = 8
+    A = G.pure_B(G.haar_unitary(k, rng), 0.8)
+    g = G.complex_gaussian(k, 0.4, rng)
+    pats = [G.random_pattern(k, int(rng.integers(0, 13)), rng) for _ in range(24)]
+    pats[3] = np.zeros(k, np.int32)                           # N = 0
+    pats[5] = np.array([2, 0, 0, 0, 0, 0, 0, 0], np.int32)   # one self-pair, eta even
+    got = tree.lhaf_rpt_batch(A, g, np.array(pats))
+    for i, reps in enumerate(pats):
+        ref, T, sabs = orc.lhaf_fds(A, g, reps)
+        check(got[i], ref, sabs)
+
+
+def test_tree_unit_ranges_bit_identical(tree):
+    # results do not depend on how the unit range is split (rank count, bench slices)
+    cfg = G.config(40)
+    rng = G.rng_for(7400)
+    reps = np.zeros(100, np.int32)
+    reps[rng.choice(100, 28, replace=False)] = 1
+    job = tree.Job(cfg["A"], cfg["gamma"], reps)
+    assert job.info.kernel == 6
+    U = job.units
+    job.reset(); job.run()
+    whole = job.finalize()[0]
+    for parts in (2, 3, 7):
+        job.reset()
+        cuts = [U * i // parts for i in range(parts + 1)]
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            job.run(a, b)
+        v = job.finalize()[0]
+        assert v == whole, (parts, v, whole)
+    job.close()
+
+
+def test_tree_n28_vs_v3(lib):
+    # d = 28 with loops: the tree and the per-term v3 kernel agree (two different algorithms)
+    cfg = G.config(40)
+    rng = G.rng_for(7500)
+    reps = np.zeros(100, np.int32)
+    reps[rng.choice(100, 28, replace=False)] = 1
+    lib.lhaf_set_kernel(6)
+    t = lib.lhaf_rpt(cfg["A"], cfg["gamma"], reps)
+    lib.lhaf_set_kernel(3)
+    v = lib.lhaf_rpt(cfg["A"], cfg["gamma"], reps)
+    lib.lhaf_set_kernel(0)
+    assert rel(t, v) <= 1e-9, (t, v)

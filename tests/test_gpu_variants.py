@@ -28,9 +28,10 @@ def refs(orc):
     return out
 
 
-@pytest.mark.parametrize("alt", [0, 3, "v5"])
+@pytest.mark.parametrize("alt", [0, 3, "v5", "tree"])
 def test_variant_block_diagonal(lib, refs, alt):
-    env = dict(os.environ, LHAF_V3_ALT=str(alt)) if alt != "v5" else dict(os.environ, LHAF_KERNEL="5")
+    env = (dict(os.environ, LHAF_KERNEL="5") if alt == "v5" else dict(os.environ, LHAF_KERNEL="6")
+           if alt == "tree" else dict(os.environ, LHAF_V3_ALT=str(alt), LHAF_KERNEL="3"))
     r = subprocess.run([sys.executable, os.path.join(HERE, "_variant_worker.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
