@@ -351,12 +351,14 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = L.lhaf_launch_count()
     with ClockSampler(local) as clk:
         e0.record(stream)
         for s in range(args.steps):
             step(s, record=True)
         e1.record(stream)
         torch.cuda.synchronize()
+    launches = L.lhaf_launch_count() - launches0
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
@@ -378,24 +380,33 @@ def main():
     full_cover = args.steps >= slices
     s_per_lhaf = (job.terms / value) if job.info.batch == 1 else None
 
-    # roofline of the dominant kernel (the sieve): algorithmic FP64 flops per launch (SURVEY
-    # 8(d)'s F per term x the launch's terms) / the launch's CUDA-event time, against the
-    # measured DFMA peak; the kernel's own executed-useful model and ncu's executed-flop
-    # fraction (profiles/, one full capture) next to it
+    # roofline of the hot path's kernels: the evaluation of a slice (job.run) is the dominant
+    # launch group (the tree's level kernels, or the per-term sieve kernel of v1/v3/v5), timed
+    # with CUDA events on the launch stream.  achieved = the kernels' algorithmic FP64 flops
+    # (job.info.flops_per_term_model: the arithmetic the variant's algorithm performs per
+    # evaluated term) x the slice's terms / event time, against the
+    # measured DFMA peak.  SURVEY 8(d)'s per-term model F (Householder + La Budde per term) is
+    # reported next to it as the equivalent throughput of the per-term method: the tree shares
+    # the Schur complements of common prefixes, so it needs far fewer flops per term than F.
     d, n = int(job.info.d_max), int(job.info.n_max)
     flops_term = survey_flops_per_term(d, n)
     own_term = job.info.flops_per_term_model
     peak, peak_src = fp64_peak()
     spec_peak = 148 * 64 * 2 * 1.965e9 / 1e12
-    achieved = my_terms * flops_term / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else None
     own = my_terms * own_term / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else None
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
+    surveyF = my_terms * flops_term / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else None
+    roofline = {"bound": "alu", "achieved": own, "peak": peak, "unit": "TFLOP/s",
+                "frac": (own / peak) if own else None, "traffic": None,
                 "peak_source": peak_src, "peak_spec": spec_peak,
-                "frac_of_spec": (achieved / spec_peak) if achieved else None,
-                "flops_per_term": flops_term, "flops_model": "SURVEY 8(d) F(d, n)",
-                "flops_per_term_kernel_useful": own_term,
-                "fp64_pct_model_kernel_useful": (own / peak) if own else None,
+                "frac_of_spec": (own / spec_peak) if own else None,
+                "flops_per_term": own_term,
+                "flops_model": ("tree (variant 6): complex MACs of the level kernels per evaluated leaf x 8"
+                                if job.info.kernel == 6 else "per-term kernel: useful FP64 flops per term"),
+                "kernels": "tree_pivot_k/tree_tmat_k/tree_update_k/tree_leaf_k/tree_reduce_k (+ tree_root_k)"
+                           if job.info.kernel == 6 else f"sieve (variant {job.info.kernel})",
+                "survey_F_per_term": flops_term,
+                "survey_F_equivalent_tflops": surveyF,
+                "survey_F_equivalent_frac": (surveyF / peak) if surveyF else None,
                 "kernel_share_of_step": kernel_ms / ms if ms > 0 else None}
     for fname, key in (("traffic.json", "traffic"), ("ncu_fp64.json", "fp64_pct_ncu")):
         fpath = os.path.join(ROOT, "profiles", fname)
@@ -479,10 +490,10 @@ def main():
             "s_per_lhaf_extrapolated": None if full_cover else s_per_lhaf,
             "result": [float(result[0]), float(result[1])] if full_cover and job.info.batch == 1 else None,
             "accuracy": {"kappa": kappa,
-                         "pin": "tests/test_gpu_fullsize.py::test_block_diagonal_N60 (P10, P:510; same kernel instance at d = 60)"},
+                         "pin": "tests/test_gpu_fullsize.py::test_block_diagonal_N60 (P10, P:510; the same default path at d = 60)"},
             "n40": n40,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": 2 * len(kernel_ev),
+            "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -250,7 +250,15 @@ typedef struct {
   uint64_t terms;        /* total evaluated terms (sum of T_eval) */
   double flops_per_term_model; /* algorithmic FP64 flops per term of the selected kernel */
   uint64_t h2d_plan_bytes;     /* bytes of plan tables copied host->device at creation */
-  int32_t precision;           /* precision mode of the job (lhaf_set_precision) */
+  int32_t precision;           /* The plan of pattern `pattern` of a job in the job's own evaluation order: the pairs and
+ * multiplicities as lhaf_plan returns them, permuted for the tree variant (the pair
+ * eliminated first is last), and T_eval = the terms the job evaluates (T when
+ * no pair has an odd count and the tree cannot halve).  Term t of lhaf_job_terms and the
+ * unit ranges of lhaf_job_run decode with this order (pair 0 fastest).  Host only.
+ * Errors: E_ARG (null pointer, pattern outside [0, batch)). */
+lhaf_status lhaf_job_plan(const lhaf_job *job, int32_t pattern, lhaf_plan_info *info);
+
+/* precision mode of the job (lhaf_set_precision) */
   int32_t pad_;
 } lhaf_job_info;
 
@@ -317,13 +325,19 @@ lhaf_status lhaf_shard_units(uint64_t units, int32_t rank, int32_t nranks, uint6
 lhaf_status lhaf_set_precision(int32_t mode);
 int32_t lhaf_get_precision(void);
 
-/* Kernel override for experiments and cross-checks: 0 = automatic (v3), 1 = the Householder
- * baseline (lhaf_kernels.cu), 3 = v3, 5 = v5 for bordered sizes 33 <= E <= 64 (v3 below) --
- * three independent reduction codes.  Errors: E_ARG for any other id. */
+/* Kernel override for experiments and cross-checks: 0 = automatic (the tree, variant 6, for
+ * plain sieves in FP64 mode; v3 for the per-term paths), 1 = the Householder baseline
+ * (lhaf_kernels.cu), 3 = v3, 5 = v5 for bordered sizes 33 <= E <= 64 (v3 below), 6 = the
+ * prefix-sharing tree (lhaf_tree.cu; plain sieves -- cutoff groups, inclusion/exclusion and
+ * gamma-batched jobs keep their per-term kernels) -- four independent codes of the same sum
+ * (DESIGN.md sections 2-3).  Errors: E_ARG for any other id. */
 lhaf_status lhaf_set_kernel(int32_t variant);
 
 const char *lhaf_last_error(void);
 const char *lhaf_version(void);
+/* Number of CUDA kernel launches the library has issued in this process (all entry points,
+ * all streams) -- a host counter, incremented at every launch site.  Never fails. */
+uint64_t lhaf_launch_count(void);
 void lhaf_shutdown(void);
 
 #ifdef __cplusplus

@@ -16,6 +16,8 @@ Parity status per function:
   matched_reps      pinned: the paper's worked example n = (2,1,0,3) -> 6 terms
   fds_term          pinned: 2x2 closed form; full-sum agreement with lhaf_brute/lhaf_et
   fds_terms         the same routine over a batch (pinned: equality with fds_term)
+  fds_sum           signed, binomially weighted fds_terms over a term range in a given pair
+                    order (pinned: whole range = lhaf_fds for a permuted pair order)
   fds_range         pinned: fds_range(0, T) 2^{-n} = lhaf_fds = lhaf_brute, additivity over a
                     split of [0, T), halving 2 sum_{t < T/2} = sum_{t < T}  (test_oracle_pins.py)
   lhaf_fds          pinned: agreement with lhaf_brute / lhaf_et, closed forms
@@ -202,8 +204,6 @@ def reduced_system(A, gamma, reps, mixed: bool = False):
     """Oracle-side reduced matrix for per-term parity: (C, v, eta, n) following reading C8
     (index list (p_1..p_H, q_1..q_H), C_ab = A_{r_a r_b} incl. diagonal, v = gamma_r,
     phantom row/col zero with loop 1).  Pure Python indexing, no arithmetic."""
-    A = _cplx(A)
-    gamma = _cplx(gamma)
     reps = np.asarray(reps, dtype=np.int32)
     if mixed:
         k = reps.shape[0]
@@ -212,13 +212,20 @@ def reduced_system(A, gamma, reps, mixed: bool = False):
         left = None
     else:
         pairs, eta, left = matched_reps(reps)
-    r = [p for p, _ in pairs]
-    s = [q for _, q in pairs]
     if left is not None:
-        r.append(left)
-        s.append(-1)
+        pairs = pairs + [(left, -1)]
         eta = eta + [1]
-    idx = r + s
+    C, v = reduced_from_pairs(A, gamma, pairs)
+    return C, v, eta, int(sum(eta))
+
+
+def reduced_from_pairs(A, gamma, pairs):
+    """(C, v) over the index list (p_1..p_H, q_1..q_H) of the given pairs (q = -1: the phantom,
+    reading C7): C_ab = A_{r_a r_b} (incl. the diagonal, reading C8), v = gamma_r (1 for the
+    phantom).  Pure Python indexing, no arithmetic."""
+    A = _cplx(A)
+    gamma = _cplx(gamma)
+    idx = [p for p, _ in pairs] + [q for _, q in pairs]
     d = len(idx)
     C = np.zeros((d, d), np.complex128)
     v = np.zeros(d, np.complex128)
@@ -227,7 +234,24 @@ def reduced_system(A, gamma, reps, mixed: bool = False):
         for b in range(d):
             if idx[a] >= 0 and idx[b] >= 0:
                 C[a, b] = A[idx[a], idx[b]]
-    return C, v, eta, int(sum(eta))
+    return C, v
+
+
+def fds_sum(C, v, eta, n: int, t0: int, t1: int, batch: int = 8192):
+    """sum_{t0 <= t < t1} (-1)^{sum k} prod C(eta_h, k_h) g(w(t)) (reading C5) over the
+    pair order of (C, v, eta): each term by fds_terms (explicit powers, long double), the
+    digits by decode.  Returns (sum, sum |term|), without the 2^{-n} prefactor."""
+    tot = 0j
+    tabs = 0.0
+    for b0 in range(t0, t1, batch):
+        ts = range(b0, min(t1, b0 + batch))
+        dec = [decode(t, eta) for t in ts]
+        W = np.array([x[1] for x in dec], np.int32)
+        g = fds_terms(C, v, W, n)
+        f = np.array([x[2] * x[3] for x in dec], np.float64)
+        tot += complex(np.sum(f * g))
+        tabs += float(np.sum(np.abs(f) * np.abs(g)))
+    return tot, tabs
 
 
 def decode(t: int, eta):

@@ -85,6 +85,7 @@ def _load() -> ctypes.CDLL:
         "lhaf_job_create": ([vp, vp, ctypes.c_int64, ip, ctypes.c_int32, ctypes.c_int32,
                              ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(vp)]),
         "lhaf_job_info_get": ([vp, ctypes.POINTER(JobInfo)]),
+        "lhaf_job_plan": ([vp, ctypes.c_int32, ctypes.POINTER(PlanInfo)]),
         "lhaf_job_reset": ([vp, vp]),
         "lhaf_job_run": ([vp, u64, u64, vp]),
         "lhaf_job_allreduce": ([vp, vp]),
@@ -111,6 +112,7 @@ def _load() -> ctypes.CDLL:
     lib.lhaf_job_destroy.restype = None
     lib.lhaf_last_error.restype = ctypes.c_char_p
     lib.lhaf_version.restype = ctypes.c_char_p
+    lib.lhaf_launch_count.restype = ctypes.c_uint64
     lib.lhaf_shutdown.restype = None
     lib.lhaf_get_precision.restype = ctypes.c_int32
     return lib
@@ -147,11 +149,12 @@ EXPORTED = ["lhaf_plan", "lhaf_decode", "lhaf_rpt", "lhaf_rpt_batch", "lhaf_rpt_
             "lhaf_rpt_multigamma",
             "lhaf_rpt_batch_dev", "lhaf_job_create", "lhaf_job_info_get", "lhaf_job_reset",
             "lhaf_job_run", "lhaf_job_allreduce", "lhaf_job_reset_range", "lhaf_job_allreduce_range",
-            "lhaf_job_finalize", "lhaf_job_abs_sum",
+            "lhaf_job_finalize", "lhaf_job_abs_sum", "lhaf_job_plan",
             "lhaf_job_partials", "lhaf_job_terms", "lhaf_job_destroy", "lhaf_set_device",
             "lhaf_get_unique_id", "lhaf_init_rank", "lhaf_rank_info", "lhaf_set_kernel",
             "lhaf_set_precision", "lhaf_get_precision",
-            "lhaf_shard_units", "lhaf_last_error", "lhaf_version", "lhaf_shutdown"]
+            "lhaf_shard_units", "lhaf_last_error", "lhaf_version", "lhaf_launch_count",
+            "lhaf_shutdown"]
 
 
 def _check(status: int):
@@ -177,6 +180,11 @@ def _ip(a: np.ndarray):
 
 def version() -> str:
     return _lib.lhaf_version().decode()
+
+
+def lhaf_launch_count() -> int:
+    """Kernel launches the library has issued in this process (bench.py's gpu_launches)."""
+    return int(_lib.lhaf_launch_count())
 
 
 def lhaf_plan(reps, mixed: int = 0) -> PlanInfo:
@@ -354,6 +362,12 @@ class Job:
     @property
     def terms(self) -> int:
         return int(self.info.terms)
+
+    def plan(self, pattern: int = 0) -> PlanInfo:
+        """The pattern's pairs / multiplicities in the job's evaluation order (lhaf_job_plan)."""
+        info = PlanInfo()
+        _check(_lib.lhaf_job_plan(self._h, pattern, ctypes.byref(info)))
+        return info
 
     def reset(self, stream: int = 0):
         _check(_lib.lhaf_job_reset(self._h, ctypes.c_void_p(stream)))

@@ -298,6 +298,7 @@ struct lhaf_job {
   // variant 6: one tree per group of patterns of the same shape
   std::vector<TreeGroup> groups;
   TreeWork tw;
+  std::vector<Plan> plans;  // per pattern, in the job's evaluation order (lhaf_job_plan)
   double tree_flops = 0.0;
   JobDev dev() const {
     JobDev J;
@@ -445,6 +446,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     }
     if (s == LHAF_OK) s = check_plan_limits(P);
     if (s != LHAF_OK) { job_free(j); return s; }
+    j->plans.push_back(P);
     PatDesc &D = j->descs[b];
     memset(&D, 0, sizeof D);
     D.d = P.d; D.H = P.H; D.n = P.n; D.flags = full ? FLAG_FULL : 0;
@@ -536,7 +538,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     }
     for (auto &g : j->groups) {
       g.npat = (int)g.pats.size();
-      tree_plan_group(g, 8192);
+      tree_plan_group(g, 65536);
       g.unit_base = unit;
       for (int32_t pb : g.pats) {
         PatDesc &D = j->descs[pb];
@@ -666,7 +668,8 @@ static lhaf_status evaluate(lhaf_job *j, double *out_host, double *out_dev, cuda
 extern "C" {
 
 const char *lhaf_last_error(void) { return g_err.c_str(); }
-const char *lhaf_version(void) { return "lhaf-b200 0.1 (sm_100a)"; }
+const char *lhaf_version(void) { return "lhaf-b200 0.2 (sm_100a)"; }
+uint64_t lhaf_launch_count(void) { return lhaf::g_launches.load(); }
 
 lhaf_status lhaf_plan(const int32_t *reps, int32_t k, int32_t mixed, lhaf_plan_info *info) {
   if (!info || (k > 0 && !reps)) return fail(LHAF_E_ARG, "null pointer argument");
@@ -750,6 +753,21 @@ lhaf_status lhaf_job_info_get(const lhaf_job *j, lhaf_job_info *info) {
                                                        : flops_per_term(j->variant, D.d, D.n, true);
       break;
     }
+  return LHAF_OK;
+}
+
+lhaf_status lhaf_job_plan(const lhaf_job *j, int32_t pattern, lhaf_plan_info *info) {
+  if (!j || !info) return fail(LHAF_E_ARG, "null pointer");
+  if (pattern < 0 || pattern >= (int32_t)j->plans.size())
+    return fail(LHAF_E_ARG, "pattern %d outside the job's %d", pattern, (int)j->plans.size());
+  const Plan &P = j->plans[pattern];
+  memset(info, 0, sizeof *info);
+  info->N = P.N; info->H = P.H; info->d = P.d; info->n = P.n; info->leftover = P.leftover;
+  info->T = P.T;
+  info->T_eval = P.T_eval;
+  for (int h = 0; h < P.H && h < LHAF_MAX_PAIRS; ++h) {
+    info->p[h] = P.p[h]; info->q[h] = P.q[h]; info->eta[h] = P.eta[h];
+  }
   return LHAF_OK;
 }
 

@@ -4,9 +4,13 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <vector>
 
 namespace lhaf {
+
+// kernel launches issued by the library (lhaf_launch_count; bench.py's gpu_launches)
+extern std::atomic<unsigned long long> g_launches;
 
 // One pattern of a job.  All offsets index the job's device pools.
 struct PatDesc {
@@ -125,7 +129,7 @@ struct TreeGroup {            // patterns that share one tree shape
   uint64_t units_pp = 0;      // units per pattern = nodes at depth k_u
 };
 struct TreeWork {             // device buffers of the tree driver, kept across calls
-  static constexpr size_t kLevelBudget = (size_t)192 << 20;  // bytes per depth
+  static constexpr size_t kLevelBudget = (size_t)512 << 20;  // bytes per depth
   std::vector<tree::TLevel> lv;
   std::vector<size_t> kbytes, lbytes, cbytes;
   void *scratch = nullptr, *val = nullptr, *absv = nullptr;

@@ -18,6 +18,8 @@
 
 namespace lhaf {
 
+std::atomic<unsigned long long> g_launches{0};
+
 #define FULL LHAF_FULL
 
 // ================================================================ variant 1 (generic)
@@ -423,6 +425,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(JobDev J, double2 *out, d
 cudaError_t launch_prep(const JobDev &job, int, cudaStream_t s) {
   if (job.npat == 0) return cudaSuccess;
   const int blocks = (job.npat + 3) / 4;
+  ++lhaf::g_launches;
   prep_kernel<<<blocks, 128, 0, s>>>(job);
   return cudaGetLastError();
 }
@@ -453,18 +456,21 @@ cudaError_t launch_sieve(const JobDev &job, int variant, int dmax, int nmax, uin
   if (grid > units) grid = units;
   e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
+  ++lhaf::g_launches;
   sieve_v1<<<(unsigned)grid, 32 * W, smem, s>>>(job, ubeg, uend, dmax, nmax, per);
   return cudaGetLastError();
 }
 
 cudaError_t launch_prep_bordered(const JobDev &job, cudaStream_t s) {
   if (job.npat == 0) return cudaSuccess;
+  ++lhaf::g_launches;
   prep_bordered<<<(job.npat + 3) / 4, 128, 0, s>>>(job);
   return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const JobDev &job, double2 *out, double *abs_out, cudaStream_t s) {
   if (job.npat == 0) return cudaSuccess;
+  ++lhaf::g_launches;
   finalize_kernel<<<job.npat, 128, 0, s>>>(job, out, abs_out);
   return cudaGetLastError();
 }
@@ -475,6 +481,7 @@ cudaError_t launch_terms(const JobDev &job, int, int dmax, int nmax, const uint6
   const size_t smem = (size_t)v1_words(dmax, nmax) * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(terms_v1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  ++lhaf::g_launches;
   terms_v1<<<nt < 1024 ? nt : 1024, 32, smem, s>>>(job, t, nt, g_out, dmax, nmax);
   return cudaGetLastError();
 }

@@ -23,13 +23,21 @@
 // series is truncated at lam^n (L = n + 1 coefficients).  Halving (term(t) = term(T-1-t),
 // reading C6) keeps the first (eta+1)/2 digits of the root pair (odd eta).
 //
-// Layout (HBM): a level buffer holds the nodes of one depth, structure-of-arrays with the node
-// index fastest -- K[(s * NE + e) * cap + node] (coefficient s, packed lower-triangle entry
-// e = i(i+1)/2 + j, j <= i), logc[s * cap + node], coef[node] -- so that threads working on
-// consecutive nodes (or consecutive children of one parent) read consecutive addresses.  Index
-// layout inside a node: [border] p_0 q_0 p_1 q_1 ...: the pair eliminated next is the last two
-// indices, and a child's matrix is the leading block of its parent's (the same packed prefix).
+// Layout (HBM): a level buffer holds the nodes of one depth, node-major with each series
+// contiguous -- K[(node * NE + e) * L + s] (packed lower-triangle entry e = i(i+1)/2 + j, j <= i,
+// coefficient s), logc[node * L + s], coef[node].  Index layout inside a node: [border] p_0 q_0
+// p_1 q_1 ...: the pair eliminated next is the last two indices, so a child's matrix is the
+// leading block of its parent's (the same packed prefix), and the two columns (u, x) of the
+// eliminated pair restricted to the live indices are the first Ep entries of the parent's last
+// two packed rows -- two contiguous runs of Ep * L coefficients.
+//
+// Kernels per depth transition: tree_pivot (thread per child: D, 1/D, log D, Q; series in
+// registers for L <= 40), tree_bc (a block per group of children: the parent's (u, x) rows and
+// the children's Q staged in shared memory, then T = Q (u, x)^T and the update K' = K + lam (u T1
+// + x T2) from shared memory); the last pair: tree_leaf (thread per node, both leaves, the
+// exp-series coefficient); tree_reduce (one block per work unit).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -38,7 +46,10 @@
 namespace lhaf {
 namespace tree {
 
-constexpr int TB = 8;  // output block of the blocked truncated series products
+#ifndef LHAF_TREE_TB
+#define LHAF_TREE_TB 8
+#endif
+constexpr int TB = LHAF_TREE_TB;  // output block of the blocked truncated series products
 
 struct SR {  // series view: element s at p[s * st]
   const double2 *p;
@@ -212,174 +223,434 @@ __device__ __forceinline__ void pivot(const SR &Kaa, const SR &Kbb, const SR &Ka
   (void)Rcopy;
 }
 
+
+// ================================================================ register-array series (L <= LM)
+// Series of length L <= LM held in registers (compile-time indices, fully unrolled loops with
+// uniform early exits at runtime L).  One operand may stream from memory (a[s], contiguous).
+
+template <int LM>
+__device__ __forceinline__ void rz(double2 (&A)[LM]) {
+#pragma unroll
+  for (int t = 0; t < LM; ++t) A[t] = c0();
+}
+template <int LM>
+__device__ __forceinline__ void rload(double2 (&A)[LM], const double2 *p, int L) {
+#pragma unroll
+  for (int t = 0; t < LM; ++t) A[t] = (t < L) ? p[t] : c0();
+}
+template <int LM>
+__device__ __forceinline__ void rstore(double2 *p, const double2 (&A)[LM], int L) {
+#pragma unroll
+  for (int t = 0; t < LM; ++t)
+    if (t < L) p[t] = A[t];
+}
+// acc[t] (+/-)= sum_{s + q + SH = t} a[s] B[q]  for t < L  (a streamed, B in registers).
+// Entries t >= L are never read: computing them (zero-padded operands) is harmless, so the
+// inner loops run to LM - 1 - s - SH with one uniform guard per s.
+template <int LM, int SH, bool NEG>
+__device__ __forceinline__ void rs_acc(double2 (&acc)[LM], const double2 *__restrict__ a, const double2 (&B)[LM],
+                                       int L) {
+#pragma unroll
+  for (int s = 0; s + SH < LM; ++s) {
+    if (s + SH < L) {
+      double2 av = a[s];
+      if (NEG) av = make_double2(-av.x, -av.y);
+#pragma unroll
+      for (int q = 0; q + s + SH < LM; ++q) acc[q + s + SH] = cfma(av, B[q], acc[q + s + SH]);
+    }
+  }
+}
+// acc[t] += sum_{s + q = t} A[s] B[q] (both in registers; zero beyond L)
+template <int LM>
+__device__ __forceinline__ void rr_acc(double2 (&acc)[LM], const double2 (&A)[LM], const double2 (&B)[LM], int L) {
+#pragma unroll
+  for (int s = 0; s < LM; ++s) {
+    if (s < L) {
+#pragma unroll
+      for (int q = 0; q + s < LM; ++q) acc[q + s] = cfma(A[s], B[q], acc[q + s]);
+    }
+  }
+}
+// R = 1/D (D[0] = 1; D zero beyond L)
+template <int LM>
+__device__ __forceinline__ void rrecip(double2 (&R)[LM], const double2 (&D)[LM], int L) {
+  R[0] = c1();
+#pragma unroll
+  for (int t = 1; t < LM; ++t) {
+    double2 x = c0();
+    if (t < L) {
+#pragma unroll
+      for (int s = 1; s <= t; ++s) x = cfma(D[s], R[t - s], x);
+    }
+    R[t] = make_double2(-x.x, -x.y);
+  }
+}
+// D <- t log D_t = sum_{s=1}^{t} s D_s R_{t-s}, in place (descending t), D[0] <- 0
+template <int LM>
+__device__ __forceinline__ void rtlog_inplace(double2 (&D)[LM], const double2 (&R)[LM], int L) {
+#pragma unroll
+  for (int s = 1; s < LM; ++s) D[s] = cscale(D[s], (double)s);
+#pragma unroll
+  for (int t = LM - 1; t >= 1; --t) {
+    double2 x = c0();
+    if (t < L) {
+#pragma unroll
+      for (int s = 1; s <= t; ++s) x = cfma(D[s], R[t - s], x);
+    }
+    D[t] = x;
+  }
+  D[0] = c0();
+}
+// E = exp(phi) from Psi_j = j phi_j (Psi[0] ignored): m E_m = sum_{j=1}^{m} Psi_j E_{m-j}
+template <int LM>
+__device__ __forceinline__ void rexp(double2 (&E)[LM], const double2 (&Psi)[LM], int L) {
+  E[0] = c1();
+#pragma unroll
+  for (int m = 1; m < LM; ++m) {
+    double2 x = c0();
+    if (m < L) {
+#pragma unroll
+      for (int j = 1; j <= m; ++j) x = cfma(Psi[j], E[m - j], x);
+    }
+    E[m] = cscale(x, 1.0 / m);
+  }
+}
+// A = D_w = 1 - 2 w lam Kab + w^2 lam^2 Delta (Kab, Delta streamed; zero beyond L)
+template <int LM>
+__device__ __forceinline__ void rdet(double2 (&A)[LM], const double2 *Kab, const double2 *Dl, int w, int L) {
+  const double wd = (double)w, w2 = wd * wd;
+#pragma unroll
+  for (int t = 0; t < LM; ++t) {
+    double2 d = (t == 0) ? c1() : c0();
+    if (t < L && w != 0) {
+      if (t >= 1) { const double2 k = Kab[t - 1]; d.x -= 2.0 * wd * k.x; d.y -= 2.0 * wd * k.y; }
+      if (t >= 2) { const double2 q = Dl[t - 2]; d.x += w2 * q.x; d.y += w2 * q.y; }
+    }
+    A[t] = d;
+  }
+}
+
+// ================================================================ kernels
 struct TStep {  // parent depth k -> children at depth k + 1, one chunk of children
   TLevel par, ch;
   uint64_t pbase;  // global index of the parent buffer's slot 0
   uint64_t c0;     // global index of the first child (slot 0 of the child buffer)
   uint64_t nc;     // children in the chunk
   int L, E, b, dmin, eta;
-  double2 *Q;  // [3][L][nc]
-  double2 *T;  // [2][L][E-2][nc]
-  double2 *S;  // [3][L][nc]
+  double2 *Q;      // [nc][3][L]: q11, q12, q22 of every child
+  double2 *S;      // fallback scratch
+  double2 *T;      // fallback T: [nc][2][E-2][L]
+  int G;           // children per block of tree_bc_k
 };
 
-__global__ void __launch_bounds__(128) tree_pivot_k(TStep P) {
+__device__ __forceinline__ void child_of(const TStep &P, uint64_t i, uint64_t &ps, int &kh, int &w) {
+  const uint64_t c = P.c0 + i, pg = c / P.b;
+  ps = pg - P.pbase;
+  kh = P.dmin + (int)(c - pg * P.b);
+  w = P.eta - 2 * kh;
+}
+
+// D = 1 - 2 w lam K_ab + w^2 lam^2 (K_ab^2 - K_aa K_bb), R = 1/D, t log D_t, Q; series in registers.
+template <int LM>
+__global__ void __launch_bounds__(128) tree_pivot_r(TStep P) {
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
   if (i >= P.nc) return;
-  const uint64_t c = P.c0 + i, pg = c / P.b, ps = pg - P.pbase;
-  const int kh = P.dmin + (int)(c - pg * P.b), w = P.eta - 2 * kh;
+  uint64_t ps; int kh, w;
+  child_of(P, i, ps, kh, w);
   const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
-  const int64_t kst = (int64_t)NE * P.par.cap;
-  const SR Kaa{P.par.K + (int64_t)tri(a, a) * P.par.cap + ps, kst};
-  const SR Kbb{P.par.K + (int64_t)tri(b, b) * P.par.cap + ps, kst};
-  const SR Kab{P.par.K + (int64_t)tri(b, a) * P.par.cap + ps, kst};
-  const int64_t st = (int64_t)P.nc;
-  pivot(Kaa, Kbb, Kab, L, w, P.S + i, P.Q + i, st, SR{P.par.logc + ps, (int64_t)P.par.cap},
-        P.ch.logc + i, (int64_t)P.ch.cap, nullptr, nullptr);
+  const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
+  const double2 *Kaa = Kp + (int64_t)tri(a, a) * L, *Kbb = Kp + (int64_t)tri(b, b) * L,
+                *Kab = Kp + (int64_t)tri(b, a) * L;
+  const double2 *lp = P.par.logc + (int64_t)ps * L;
+  double2 *lc = P.ch.logc + (int64_t)i * L;
+  double2 *Q = P.Q + (int64_t)i * 3 * L;
+  const double wd = (double)w, w2 = wd * wd;
+  double2 A[LM], B[LM];
+  if (w == 0) {  // deleted pair: D = 1, Q = 0
+    for (int t = 0; t < L; ++t) { lc[t] = lp[t]; Q[t] = Q[L + t] = Q[2 * L + t] = c0(); }
+  } else {
+    rload(A, Kab, L);
+    rz(B);
+    rr_acc(B, A, A, L);                 // Kab^2
+    rload(A, Kaa, L);
+    rs_acc<LM, 0, true>(B, Kbb, A, L);  // - Kaa Kbb
+    // rdet streams Delta from memory; keep it in registers instead: A = D from B
+#pragma unroll
+    for (int t = LM - 1; t >= 0; --t) {
+      double2 d = (t == 0) ? c1() : c0();
+      if (t < L) {
+        if (t >= 1) { const double2 k = Kab[t - 1]; d.x -= 2.0 * wd * k.x; d.y -= 2.0 * wd * k.y; }
+        if (t >= 2) { d.x += w2 * B[t - 2].x; d.y += w2 * B[t - 2].y; }
+      }
+      A[t] = d;
+    }
+    rrecip(B, A, L);                    // B = R
+    rtlog_inplace(A, B, L);             // A = t log D_t
+#pragma unroll
+    for (int t = 0; t < LM; ++t)
+      if (t < L) lc[t] = t ? cadd(lp[t], cscale(A[t], 1.0 / t)) : lp[t];
+    rz(A);
+    rs_acc<LM, 1, false>(A, Kbb, B, L);
+#pragma unroll
+    for (int t = 0; t < LM; ++t)
+      if (t < L) Q[t] = cscale(A[t], w2);                      // q11 = lam w^2 Kbb R
+    rz(A);
+    rs_acc<LM, 1, false>(A, Kaa, B, L);
+#pragma unroll
+    for (int t = 0; t < LM; ++t)
+      if (t < L) Q[2 * L + t] = cscale(A[t], w2);              // q22 = lam w^2 Kaa R
+    rz(A);
+    rs_acc<LM, 1, false>(A, Kab, B, L);
+#pragma unroll
+    for (int t = 0; t < LM; ++t)
+      if (t < L) Q[L + t] = make_double2(wd * B[t].x - w2 * A[t].x, wd * B[t].y - w2 * A[t].y);  // q12
+  }
   P.ch.coef[i] = P.par.coef[ps] * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
 }
 
-// T_j = Q (u_j, x_j)^T for every live index j of every child (thread per (j, child))
-__global__ void __launch_bounds__(128) tree_tmat_k(TStep P) {
+// generic pivot (any L): the blocked series routines above with per-child scratch in HBM
+__global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
+  const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
+  if (i >= P.nc) return;
+  uint64_t ps; int kh, w;
+  child_of(P, i, ps, kh, w);
+  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
+  const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
+  pivot(SR{Kp + (int64_t)tri(a, a) * L, 1}, SR{Kp + (int64_t)tri(b, b) * L, 1}, SR{Kp + (int64_t)tri(b, a) * L, 1},
+        L, w, P.S + (int64_t)i * 3 * L, P.Q + (int64_t)i * 3 * L, 1, SR{P.par.logc + (int64_t)ps * L, 1},
+        P.ch.logc + (int64_t)i * L, 1, nullptr, nullptr);
+  P.ch.coef[i] = P.par.coef[ps] * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
+}
+
+// T_j = Q (u_j, x_j)^T and K'_ij = K_ij + lam (u_i T1_j + x_i T2_j) for a group of G children:
+// the parent rows (u, x) and the children's Q in shared memory, T written there, then the
+// packed lower triangle of every child.  Shared layout per child: U[Ep][L] X[Ep][L] Q[3][L]
+// T1[Ep][L] T2[Ep][L].
+__global__ void __launch_bounds__(128) tree_bc_k(TStep P) {
+  extern __shared__ double2 sm[];
+  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1, Ep = E - 2;
+  const int NEc = Ep * (Ep + 1) / 2;
+  const int per = (4 * Ep + 3) * L;
+  const uint64_t g0 = (uint64_t)blockIdx.x * P.G;
+  const int G = (int)min((uint64_t)P.G, P.nc - g0);
+  const int tid = threadIdx.x;
+  // stage
+  for (int g = 0; g < G; ++g) {
+    uint64_t ps; int kh, w;
+    child_of(P, g0 + g, ps, kh, w);
+    const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
+    const double2 *ur = Kp + (int64_t)tri(a, 0) * L, *xr = Kp + (int64_t)tri(b, 0) * L;
+    const double2 *qr = P.Q + (int64_t)(g0 + g) * 3 * L;
+    double2 *base = sm + (int64_t)g * per;
+    for (int t = tid; t < Ep * L; t += 128) { base[t] = ur[t]; base[Ep * L + t] = xr[t]; }
+    for (int t = tid; t < 3 * L; t += 128) base[2 * Ep * L + t] = qr[t];
+  }
+  __syncthreads();
+  const int Lo = L - 1;
+  for (int task = tid; task < G * 2 * Ep; task += 128) {
+    const int g = task / (2 * Ep), r = task - g * 2 * Ep, j = r >> 1, which = r & 1;
+    double2 *base = sm + (int64_t)g * per;
+    const double2 *U = base, *X = base + Ep * L, *Qs = base + 2 * Ep * L;
+    double2 *T = base + (2 * Ep + 3) * L + (int64_t)which * Ep * L + (int64_t)j * L;
+    // T1 = q11 u + q12 x ; T2 = q12 u + q22 x
+    const SR qa{Qs + (which ? L : 0), 1}, qb{Qs + (which ? 2 * L : L), 1};
+    for (int t0 = 0; t0 < Lo; t0 += TB) {
+      double2 acc[TB];
+#pragma unroll
+      for (int k = 0; k < TB; ++k) acc[k] = c0();
+      conv_acc(acc, t0, 0, qa, Lo, SR{U + (int64_t)j * L, 1}, Lo);
+      conv_acc(acc, t0, 0, qb, Lo, SR{X + (int64_t)j * L, 1}, Lo);
+#pragma unroll
+      for (int k = 0; k < TB; ++k)
+        if (t0 + k < Lo) T[t0 + k] = acc[k];
+    }
+  }
+  __syncthreads();
+  for (int task = tid; task < G * NEc; task += 128) {
+    const int g = task / NEc, e = task - g * NEc;
+    int ii = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (tri(ii + 1, 0) <= e) ++ii;
+    while (tri(ii, 0) > e) --ii;
+    const int jj = e - tri(ii, 0);
+    uint64_t ps; int kh, w;
+    child_of(P, g0 + g, ps, kh, w);
+    const double2 *base = sm + (int64_t)g * per;
+    const double2 *U = base, *X = base + Ep * L, *T1 = base + (2 * Ep + 3) * L, *T2 = T1 + Ep * L;
+    const double2 *K = P.par.K + ((int64_t)ps * NE + e) * L;
+    double2 *out = P.ch.K + ((int64_t)(g0 + g) * NEc + e) * L;
+    for (int t0 = 0; t0 < L; t0 += TB) {
+      double2 acc[TB];
+#pragma unroll
+      for (int k = 0; k < TB; ++k) acc[k] = (t0 + k < L) ? K[t0 + k] : c0();
+      conv_acc(acc, t0, 1, SR{U + (int64_t)ii * L, 1}, Lo, SR{T1 + (int64_t)jj * L, 1}, Lo);
+      conv_acc(acc, t0, 1, SR{X + (int64_t)ii * L, 1}, Lo, SR{T2 + (int64_t)jj * L, 1}, Lo);
+#pragma unroll
+      for (int k = 0; k < TB; ++k)
+        if (t0 + k < L) out[t0 + k] = acc[k];
+    }
+  }
+}
+
+// fallback when a child group's rows do not fit shared memory: T in HBM, then the update
+__global__ void __launch_bounds__(128) tree_tmat_g(TStep P) {
   const int Ep = P.E - 2;
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
   if (i >= P.nc * (uint64_t)Ep) return;
-  const uint64_t ci = i % P.nc;
-  const int j = (int)(i / P.nc);
-  const uint64_t ps = (P.c0 + ci) / P.b - P.pbase;
-  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
-  const int64_t kst = (int64_t)NE * P.par.cap, st = (int64_t)P.nc;
-  const SR u{P.par.K + (int64_t)tri(a, j) * P.par.cap + ps, kst};
-  const SR x{P.par.K + (int64_t)tri(b, j) * P.par.cap + ps, kst};
-  const SR q11{P.Q + ci, st}, q12{P.Q + (int64_t)L * st + ci, st}, q22{P.Q + 2 * (int64_t)L * st + ci, st};
-  double2 *T1 = P.T + (int64_t)j * st + ci, *T2 = P.T + ((int64_t)L * Ep + j) * st + ci;
-  const int64_t tst = (int64_t)Ep * st;
-  const int Lo = L - 1;  // T enters K' at lam^1: degrees <= L - 2
+  const uint64_t ci = i / Ep;
+  const int j = (int)(i - ci * Ep);
+  uint64_t ps; int kh, w;
+  child_of(P, ci, ps, kh, w);
+  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1, Lo = L - 1;
+  const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
+  const SR u{Kp + (int64_t)tri(a, j) * L, 1}, x{Kp + (int64_t)tri(b, j) * L, 1};
+  const double2 *Qs = P.Q + (int64_t)ci * 3 * L;
+  double2 *T1 = P.T + ((int64_t)ci * 2 * Ep + j) * L, *T2 = T1 + (int64_t)Ep * L;
   for (int t0 = 0; t0 < Lo; t0 += TB) {
     double2 a1[TB], a2[TB];
 #pragma unroll
     for (int k = 0; k < TB; ++k) a1[k] = a2[k] = c0();
-    conv_acc(a1, t0, 0, q11, Lo, u, Lo);
-    conv_acc(a1, t0, 0, q12, Lo, x, Lo);
-    conv_acc(a2, t0, 0, q12, Lo, u, Lo);
-    conv_acc(a2, t0, 0, q22, Lo, x, Lo);
+    conv_acc(a1, t0, 0, SR{Qs, 1}, Lo, u, Lo);
+    conv_acc(a1, t0, 0, SR{Qs + L, 1}, Lo, x, Lo);
+    conv_acc(a2, t0, 0, SR{Qs + L, 1}, Lo, u, Lo);
+    conv_acc(a2, t0, 0, SR{Qs + 2 * L, 1}, Lo, x, Lo);
 #pragma unroll
     for (int k = 0; k < TB; ++k)
-      if (t0 + k < Lo) {
-        T1[(int64_t)(t0 + k) * tst] = a1[k];
-        T2[(int64_t)(t0 + k) * tst] = a2[k];
-      }
+      if (t0 + k < Lo) { T1[t0 + k] = a1[k]; T2[t0 + k] = a2[k]; }
   }
 }
-
-// K'_ij = K_ij + lam (u_i T1_j + x_i T2_j) for the packed lower triangle of every child
-__global__ void __launch_bounds__(128) tree_update_k(TStep P) {
+__global__ void __launch_bounds__(128) tree_update_g(TStep P) {
   const int Ep = P.E - 2, NEc = Ep * (Ep + 1) / 2;
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
   if (i >= P.nc * (uint64_t)NEc) return;
-  const uint64_t ci = i % P.nc;
-  const int e = (int)(i / P.nc);
+  const uint64_t ci = i / NEc;
+  const int e = (int)(i - ci * NEc);
   int ii = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
   while (tri(ii + 1, 0) <= e) ++ii;
   while (tri(ii, 0) > e) --ii;
   const int jj = e - tri(ii, 0);
-  const uint64_t ps = (P.c0 + ci) / P.b - P.pbase;
-  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
-  const int64_t kst = (int64_t)NE * P.par.cap, st = (int64_t)P.nc, tst = (int64_t)Ep * st;
-  const SR u{P.par.K + (int64_t)tri(a, ii) * P.par.cap + ps, kst};
-  const SR x{P.par.K + (int64_t)tri(b, ii) * P.par.cap + ps, kst};
-  const SR K{P.par.K + (int64_t)e * P.par.cap + ps, kst};
-  const SR T1{P.T + (int64_t)jj * st + ci, tst}, T2{P.T + ((int64_t)L * Ep + jj) * st + ci, tst};
-  double2 *out = P.ch.K + (int64_t)e * P.ch.cap + ci;
-  const int64_t ost = (int64_t)NEc * P.ch.cap;
+  uint64_t ps; int kh, w;
+  child_of(P, ci, ps, kh, w);
+  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1, Lo = L - 1;
+  const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
+  const SR u{Kp + (int64_t)tri(a, ii) * L, 1}, x{Kp + (int64_t)tri(b, ii) * L, 1};
+  const double2 *T1 = P.T + ((int64_t)ci * 2 * Ep + jj) * L, *T2 = T1 + (int64_t)Ep * L;
+  const double2 *K = Kp + (int64_t)e * L;
+  double2 *out = P.ch.K + ((int64_t)ci * NEc + e) * L;
   for (int t0 = 0; t0 < L; t0 += TB) {
     double2 acc[TB];
 #pragma unroll
-    for (int k = 0; k < TB; ++k) acc[k] = (t0 + k < L) ? at(K, t0 + k) : c0();
-    conv_acc(acc, t0, 1, u, L - 1, T1, L - 1);
-    conv_acc(acc, t0, 1, x, L - 1, T2, L - 1);
+    for (int k = 0; k < TB; ++k) acc[k] = (t0 + k < L) ? K[t0 + k] : c0();
+    conv_acc(acc, t0, 1, u, Lo, SR{T1, 1}, Lo);
+    conv_acc(acc, t0, 1, x, Lo, SR{T2, 1}, Lo);
 #pragma unroll
     for (int k = 0; k < TB; ++k)
-      if (t0 + k < L) out[(int64_t)(t0 + k) * ost] = acc[k];
+      if (t0 + k < L) out[t0 + k] = acc[k];
   }
 }
 
 struct TLeaf {
   TLevel par;      // nodes at depth H-1 (one pair left, plus the border)
-  uint64_t pbase;  // global index of slot 0 (= first node of the chunk)
   uint64_t np;     // nodes in the chunk
   int L, E, bord, b, dmin, eta;
-  double2 *S;      // scratch [9][L][np]
+  double2 *S;      // scratch [np][9][L]
   double2 *val;    // [np]: sum over the node's leaves of sign * prod C * g
   double *absv;    // [np]: the same sum of |.|
 };
 
-// The last pair of every node: its (eta + 1) leaves (or the halved root digits when H = 1).
-__global__ void __launch_bounds__(128) tree_leaf_k(TLeaf P) {
+// The last pair of every node, both (all) digits; the node-level products shared by the leaves:
+// Delta = K_ab^2 - K_aa K_bb, and with the border P = u (K_bb u - K_ab x) + x (K_aa x - K_ab u)
+// and N0 = u x, so that the leaf's border entry is K'_00 = K_00 + lam R_w (lam w^2 P + 2 w N0).
+template <int LM>
+__global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
   if (i >= P.np) return;
   const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
-  const int64_t kst = (int64_t)NE * P.par.cap, st = (int64_t)P.np;
-  const SR Kaa{P.par.K + (int64_t)tri(a, a) * P.par.cap + i, kst};
-  const SR Kbb{P.par.K + (int64_t)tri(b, b) * P.par.cap + i, kst};
-  const SR Kab{P.par.K + (int64_t)tri(b, a) * P.par.cap + i, kst};
-  const SR logc{P.par.logc + i, (int64_t)P.par.cap};
-  double2 *S = P.S + i;                                   // D, R, sD
-  double2 *Qo = P.S + 3 * (int64_t)L * st + i;            // q11, q12, q22
-  double2 *Psi = P.S + 6 * (int64_t)L * st + i;           // t log D_t, then Psi
-  double2 *T1 = P.S + 7 * (int64_t)L * st + i, *T2 = P.S + 8 * (int64_t)L * st + i;
+  const double2 *Kp = P.par.K + (int64_t)i * NE * L;
+  const double2 *Kaa = Kp + (int64_t)tri(a, a) * L, *Kbb = Kp + (int64_t)tri(b, b) * L,
+                *Kab = Kp + (int64_t)tri(b, a) * L;
+  const double2 *lc = P.par.logc + (int64_t)i * L;
+  double2 *S0 = P.S + (int64_t)i * 4 * L, *S1 = S0 + L, *S2 = S1 + L, *S3 = S2 + L;
+  double2 A[LM], B[LM];
+  // Delta -> S0
+  rload(A, Kab, L);
+  rz(B);
+  rr_acc(B, A, A, L);
+  rload(A, Kaa, L);
+  rs_acc<LM, 0, true>(B, Kbb, A, L);
+  rstore(S0, B, L);
+  const double2 *u = nullptr, *x = nullptr, *K00 = nullptr;
+  if (P.bord) {
+    u = Kp + (int64_t)tri(a, 0) * L;
+    x = Kp + (int64_t)tri(b, 0) * L;
+    K00 = Kp;
+    rload(A, u, L);                      // P1 = Kbb u - Kab x -> S1
+    rz(B);
+    rs_acc<LM, 0, false>(B, Kbb, A, L);
+    rload(A, x, L);
+    rs_acc<LM, 0, true>(B, Kab, A, L);
+    rstore(S1, B, L);
+    rz(B);                               // P2 = Kaa x - Kab u -> S2
+    rs_acc<LM, 0, false>(B, Kaa, A, L);
+    rload(A, u, L);
+    rs_acc<LM, 0, true>(B, Kab, A, L);
+    rstore(S2, B, L);
+    rz(B);                               // P = u P1 + x P2 -> S1
+    rs_acc<LM, 0, false>(B, S1, A, L);
+    rload(A, x, L);
+    rs_acc<LM, 0, false>(B, S2, A, L);
+    rstore(S1, B, L);
+    rz(B);                               // N0 = u x -> S2
+    rs_acc<LM, 0, false>(B, u, A, L);
+    rstore(S2, B, L);
+  }
   const double coef = P.par.coef[i];
   double2 vsum = c0();
   double asum = 0.0;
   for (int d = 0; d < P.b; ++d) {
     const int kh = P.dmin + d, w = P.eta - 2 * kh;
-    pivot(Kaa, Kbb, Kab, L, w, S, P.bord ? Qo : nullptr, st, logc, nullptr, 0, Psi, nullptr);
-    // Psi_t = t phi_t, phi = 1/2 (K'_00 - log c - log D)
+    const double wd = (double)w, w2 = wd * wd;
+    rdet(A, Kab, S0, w, L);              // A = D_w
+    rrecip(B, A, L);                     // B = R_w
+    rtlog_inplace(A, B, L);              // A = t log D_w
     if (P.bord) {
-      const SR u{P.par.K + (int64_t)tri(a, 0) * P.par.cap + i, kst};
-      const SR x{P.par.K + (int64_t)tri(b, 0) * P.par.cap + i, kst};
-      const SR q11{Qo, st}, q12{Qo + (int64_t)L * st, st}, q22{Qo + 2 * (int64_t)L * st, st};
-      const int Lo = L - 1;
-      for (int t0 = 0; t0 < Lo; t0 += TB) {
-        double2 a1[TB], a2[TB];
+      rstore(S3, A, L);
+      // A = R_w (lam w^2 P + 2 w N0): stream N_w[s] = w^2 P[s-1] + 2 w N0[s]
+      rz(A);
 #pragma unroll
-        for (int k = 0; k < TB; ++k) a1[k] = a2[k] = c0();
-        conv_acc(a1, t0, 0, q11, Lo, u, Lo);
-        conv_acc(a1, t0, 0, q12, Lo, x, Lo);
-        conv_acc(a2, t0, 0, q12, Lo, u, Lo);
-        conv_acc(a2, t0, 0, q22, Lo, x, Lo);
+      for (int s = 0; s < LM; ++s) {
+        if (s < L) {
+          double2 nv = cscale(S2[s], 2.0 * wd);
+          if (s >= 1) { const double2 pv = S1[s - 1]; nv.x += w2 * pv.x; nv.y += w2 * pv.y; }
 #pragma unroll
-        for (int k = 0; k < TB; ++k)
-          if (t0 + k < Lo) {
-            T1[(int64_t)(t0 + k) * st] = a1[k];
-            T2[(int64_t)(t0 + k) * st] = a2[k];
-          }
-      }
-      const SR K00{P.par.K + i, kst};
-      for (int t0 = 0; t0 < L; t0 += TB) {
-        double2 acc[TB];
-#pragma unroll
-        for (int k = 0; k < TB; ++k) acc[k] = (t0 + k < L) ? at(K00, t0 + k) : c0();
-        conv_acc(acc, t0, 1, u, Lo, SR{T1, st}, Lo);
-        conv_acc(acc, t0, 1, x, Lo, SR{T2, st}, Lo);
-#pragma unroll
-        for (int k = 0; k < TB; ++k) {
-          const int t = t0 + k;
-          if (t < L) {
-            const double2 k00 = acc[k], lc = at(logc, t), tl = Psi[(int64_t)t * st];
-            Psi[(int64_t)t * st] = make_double2(0.5 * (t * (k00.x - lc.x) - tl.x), 0.5 * (t * (k00.y - lc.y) - tl.y));
-          }
+          for (int q = 0; q + s < LM; ++q) A[q + s] = cfma(nv, B[q], A[q + s]);
         }
       }
+      // B = Psi_t = t phi_t, phi = 1/2 (K00 + lam M - log c - log D)
+#pragma unroll
+      for (int t = 0; t < LM; ++t) {
+        double2 ps = c0();
+        if (t >= 1 && t < L) {
+          const double2 k0 = K00[t], l0 = lc[t], tl = S3[t], m = A[t - 1];
+          ps = make_double2(0.5 * (t * (k0.x + m.x - l0.x) - tl.x), 0.5 * (t * (k0.y + m.y - l0.y) - tl.y));
+        }
+        B[t] = ps;
+      }
     } else {
-      for (int t = 0; t < L; ++t) {
-        const double2 lc = at(logc, t), tl = Psi[(int64_t)t * st];
-        Psi[(int64_t)t * st] = make_double2(-0.5 * (t * lc.x + tl.x), -0.5 * (t * lc.y + tl.y));
+#pragma unroll
+      for (int t = 0; t < LM; ++t) {
+        double2 ps = c0();
+        if (t >= 1 && t < L) {
+          const double2 l0 = lc[t];
+          ps = make_double2(-0.5 * (t * l0.x + A[t].x), -0.5 * (t * l0.y + A[t].y));
+        }
+        B[t] = ps;
       }
     }
-    double2 *Ev = S;  // reuse D's slots
-    ser_exp(Ev, st, Psi, L);
-    const double2 g = Ev[(int64_t)(L - 1) * st];
+    rexp(A, B, L);
+    double2 g = c0();
+#pragma unroll
+    for (int t = 0; t < LM; ++t)
+      if (t == L - 1) g = A[t];
     const double f = coef * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
     vsum.x = fma(f, g.x, vsum.x);
     vsum.y = fma(f, g.y, vsum.y);
@@ -389,40 +660,99 @@ __global__ void __launch_bounds__(128) tree_leaf_k(TLeaf P) {
   P.absv[i] = asum;
 }
 
-// Whole units of the chunk: one warp per unit sums its per-node values in a fixed order
-// (double-double) and writes the unit's partial.
-__global__ void __launch_bounds__(128) tree_reduce_k(const double2 *val, const double *absv,
-                                                     uint64_t units, uint64_t per_unit, uint64_t unit0,
-                                                     Partial *partials) {
-  const uint64_t u = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (u >= units) return;
+// generic leaf (any L): the blocked series routines with scratch in HBM
+__global__ void __launch_bounds__(128) tree_leaf_g(TLeaf P) {
+  const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
+  if (i >= P.np) return;
+  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
+  const double2 *Kp = P.par.K + (int64_t)i * NE * L;
+  const SR Kaa{Kp + (int64_t)tri(a, a) * L, 1}, Kbb{Kp + (int64_t)tri(b, b) * L, 1}, Kab{Kp + (int64_t)tri(b, a) * L, 1};
+  const SR logc{P.par.logc + (int64_t)i * L, 1};
+  double2 *S = P.S + (int64_t)i * 9 * L;
+  double2 *Qo = S + 3 * L, *Psi = S + 6 * L, *T1 = S + 7 * L, *T2 = S + 8 * L;
+  const double coef = P.par.coef[i];
+  double2 vsum = c0();
+  double asum = 0.0;
+  for (int d = 0; d < P.b; ++d) {
+    const int kh = P.dmin + d, w = P.eta - 2 * kh;
+    pivot(Kaa, Kbb, Kab, L, w, S, P.bord ? Qo : nullptr, 1, logc, nullptr, 0, Psi, nullptr);
+    if (P.bord) {
+      const SR u{Kp + (int64_t)tri(a, 0) * L, 1}, x{Kp + (int64_t)tri(b, 0) * L, 1};
+      const int Lo = L - 1;
+      for (int t0 = 0; t0 < Lo; t0 += TB) {
+        double2 a1[TB], a2[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) a1[k] = a2[k] = c0();
+        conv_acc(a1, t0, 0, SR{Qo, 1}, Lo, u, Lo);
+        conv_acc(a1, t0, 0, SR{Qo + L, 1}, Lo, x, Lo);
+        conv_acc(a2, t0, 0, SR{Qo + L, 1}, Lo, u, Lo);
+        conv_acc(a2, t0, 0, SR{Qo + 2 * L, 1}, Lo, x, Lo);
+#pragma unroll
+        for (int k = 0; k < TB; ++k)
+          if (t0 + k < Lo) { T1[t0 + k] = a1[k]; T2[t0 + k] = a2[k]; }
+      }
+      for (int t0 = 0; t0 < L; t0 += TB) {
+        double2 acc[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) acc[k] = (t0 + k < L) ? Kp[t0 + k] : c0();
+        conv_acc(acc, t0, 1, u, Lo, SR{T1, 1}, Lo);
+        conv_acc(acc, t0, 1, x, Lo, SR{T2, 1}, Lo);
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          const int t = t0 + k;
+          if (t < L) {
+            const double2 k00 = acc[k], lc = at(logc, t), tl = Psi[t];
+            Psi[t] = make_double2(0.5 * (t * (k00.x - lc.x) - tl.x), 0.5 * (t * (k00.y - lc.y) - tl.y));
+          }
+        }
+      }
+    } else {
+      for (int t = 0; t < L; ++t) {
+        const double2 lc = at(logc, t), tl = Psi[t];
+        Psi[t] = make_double2(-0.5 * (t * lc.x + tl.x), -0.5 * (t * lc.y + tl.y));
+      }
+    }
+    ser_exp(S, 1, Psi, L);
+    const double2 g = S[L - 1];
+    const double f = coef * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
+    vsum.x = fma(f, g.x, vsum.x);
+    vsum.y = fma(f, g.y, vsum.y);
+    asum += fabs(f) * hypot(g.x, g.y);
+  }
+  P.val[i] = vsum;
+  P.absv[i] = asum;
+}
+
+// Whole units of the chunk: one block per unit sums its per-node values (thread t: nodes
+// t, t + 256, ... in double-double; then a fixed-shape tree over the threads) and writes the
+// unit's partial.  The order depends only on the unit's size: results are independent of the
+// chunking and of the rank count.
+__global__ void __launch_bounds__(256) tree_reduce_k(const double2 *val, const double *absv,
+                                                     uint64_t per_unit, uint64_t unit0, Partial *partials) {
+  __shared__ double sh[6][256];
+  const uint64_t u = blockIdx.x;
+  const int t = threadIdx.x;
   double rh = 0, rl = 0, ih = 0, il = 0, ah = 0, al = 0;
-  for (uint64_t m = lane; m < per_unit; m += 32) {
+  for (uint64_t m = t; m < per_unit; m += 256) {
     const double2 v = val[u * per_unit + m];
     dd_add(rh, rl, v.x);
     dd_add(ih, il, v.y);
     dd_add(ah, al, absv[u * per_unit + m]);
   }
-#pragma unroll
-  for (int s = 16; s; s >>= 1) {
-    const double orh = __shfl_xor_sync(LHAF_FULL, rh, s), orl = __shfl_xor_sync(LHAF_FULL, rl, s);
-    const double oih = __shfl_xor_sync(LHAF_FULL, ih, s), oil = __shfl_xor_sync(LHAF_FULL, il, s);
-    const double oah = __shfl_xor_sync(LHAF_FULL, ah, s), oal = __shfl_xor_sync(LHAF_FULL, al, s);
-    // combine in a lane-order-independent way: the lower lane's value first
-    if (lane & s) {
-      double th = orh, tl = orl; dd_add_dd(th, tl, rh, rl); rh = th; rl = tl;
-      th = oih; tl = oil; dd_add_dd(th, tl, ih, il); ih = th; il = tl;
-      th = oah; tl = oal; dd_add_dd(th, tl, ah, al); ah = th; al = tl;
-    } else {
-      dd_add_dd(rh, rl, orh, orl);
-      dd_add_dd(ih, il, oih, oil);
-      dd_add_dd(ah, al, oah, oal);
+  sh[0][t] = rh; sh[1][t] = rl; sh[2][t] = ih; sh[3][t] = il; sh[4][t] = ah; sh[5][t] = al;
+  __syncthreads();
+  for (int s = 128; s; s >>= 1) {
+    if (t < s) {
+      dd_add_dd(sh[0][t], sh[1][t], sh[0][t + s], sh[1][t + s]);
+      dd_add_dd(sh[2][t], sh[3][t], sh[2][t + s], sh[3][t + s]);
+      dd_add_dd(sh[4][t], sh[5][t], sh[4][t + s], sh[5][t + s]);
     }
+    __syncthreads();
   }
-  if (lane == 0) {
+  if (t == 0) {
     Partial q;
-    q.re_hi = rh; q.re_lo = rl; q.im_hi = ih; q.im_lo = il; q.abs_hi = ah; q.abs_lo = al;
+    q.re_hi = sh[0][0]; q.re_lo = sh[1][0]; q.im_hi = sh[2][0]; q.im_lo = sh[3][0];
+    q.abs_hi = sh[4][0]; q.abs_lo = sh[5][0];
     q.pad0 = q.pad1 = 0.0;
     partials[unit0 + u] = q;
   }
@@ -434,8 +764,8 @@ __global__ void __launch_bounds__(128) tree_root_k(JobDev J, const int32_t *pats
   const int NE = E * (E + 1) / 2;
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
   if (i >= n * (uint64_t)NE) return;
-  const uint64_t slot = i % n;
-  const int e = (int)(i / n);
+  const uint64_t slot = i / NE;
+  const int e = (int)(i - slot * NE);
   int ii = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
   while (tri(ii + 1, 0) <= e) ++ii;
   while (tri(ii, 0) > e) --ii;
@@ -458,12 +788,11 @@ __global__ void __launch_bounds__(128) tree_root_k(JobDev J, const int32_t *pats
     const int mi = mode(ii), mj = mode(jj);
     if (mi >= 0 && mj >= 0) v = J.A[(int64_t)mi * J.kdim + mj];
   }
-  const int64_t st = (int64_t)NE * out.cap;
-  double2 *o = out.K + (int64_t)e * out.cap + slot;
+  double2 *o = out.K + ((int64_t)slot * NE + e) * L;
   o[0] = v;
-  for (int s = 1; s < L; ++s) o[(int64_t)s * st] = c0();
+  for (int s = 1; s < L; ++s) o[s] = c0();
   if (e == 0) {
-    for (int s = 0; s < L; ++s) out.logc[(int64_t)s * out.cap + slot] = c0();
+    for (int s = 0; s < L; ++s) out.logc[(int64_t)slot * L + s] = c0();
     out.coef[slot] = 1.0;
   }
 }
@@ -481,6 +810,14 @@ static cudaError_t grow(void **p, size_t &have, size_t need) {
 }
 
 static inline unsigned blocks_for(uint64_t n) { return (unsigned)((n + 127) / 128); }
+
+static int reg_limit() {  // LHAF_TREE_REGL: largest L for the register-array kernels (default 40)
+  static const int v = [] {
+    const char *e = getenv("LHAF_TREE_REGL");
+    return e ? atoi(e) : 40;
+  }();
+  return v;
+}
 
 struct Runner {
   const JobDev &J;
@@ -512,18 +849,23 @@ struct Runner {
     const int k = H - 1;
     TLeaf P;
     P.par = w.lv[k];
-    P.pbase = gs;
     P.np = cnt;
     P.L = L; P.E = E[k]; P.bord = g.bord; P.b = b[k]; P.dmin = dmin[k]; P.eta = eta[k];
     P.S = (double2 *)w.scratch;
     P.val = (double2 *)w.val;
     P.absv = (double *)w.absv;
-    tree_leaf_k<<<blocks_for(cnt), 128, 0, st>>>(P);
+    ++lhaf::g_launches;
+    const int rl = reg_limit();
+    if (L <= 16 && L <= rl) tree_leaf_r<16><<<blocks_for(cnt), 128, 0, st>>>(P);
+    else if (L <= 24 && L <= rl) tree_leaf_r<24><<<blocks_for(cnt), 128, 0, st>>>(P);
+    else if (L <= 32 && L <= rl) tree_leaf_r<32><<<blocks_for(cnt), 128, 0, st>>>(P);
+    else if (L <= 40 && L <= rl) tree_leaf_r<40><<<blocks_for(cnt), 128, 0, st>>>(P);
+    else tree_leaf_g<<<blocks_for(cnt), 128, 0, st>>>(P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const uint64_t per = Pk[k], units = cnt / per;
-    tree_reduce_k<<<(unsigned)((units + 3) / 4), 128, 0, st>>>(P.val, P.absv, units, per,
-                                                              g.unit_base + gs / per, J.partials);
+    ++lhaf::g_launches;
+    tree_reduce_k<<<(unsigned)units, 256, 0, st>>>(P.val, P.absv, per, g.unit_base + gs / per, J.partials);
     return cudaGetLastError();
   }
 
@@ -546,14 +888,29 @@ struct Runner {
       P.c0 = c;
       P.nc = n;
       P.L = L; P.E = E[k]; P.b = b[k]; P.dmin = dmin[k]; P.eta = eta[k];
-      const int Ep = E[k] - 2;
-      P.S = (double2 *)w.scratch;
-      P.Q = P.S + (size_t)3 * L * n;
-      P.T = P.Q + (size_t)3 * L * n;
-      tree_pivot_k<<<blocks_for(n), 128, 0, st>>>(P);
+      const int Ep = E[k] - 2, NEc = Ep * (Ep + 1) / 2;
+      P.Q = (double2 *)w.scratch;
+      P.S = P.Q + (size_t)3 * L * n;
+      P.T = P.S + (size_t)3 * L * n;
+      ++lhaf::g_launches;
+      const int rl = reg_limit();
+      if (L <= 16 && L <= rl) tree_pivot_r<16><<<blocks_for(n), 128, 0, st>>>(P);
+      else if (L <= 24 && L <= rl) tree_pivot_r<24><<<blocks_for(n), 128, 0, st>>>(P);
+      else if (L <= 32 && L <= rl) tree_pivot_r<32><<<blocks_for(n), 128, 0, st>>>(P);
+      else if (L <= 40 && L <= rl) tree_pivot_r<40><<<blocks_for(n), 128, 0, st>>>(P);
+      else tree_pivot_g<<<blocks_for(n), 128, 0, st>>>(P);
       if (Ep > 0) {
-        tree_tmat_k<<<blocks_for(n * Ep), 128, 0, st>>>(P);
-        tree_update_k<<<blocks_for(n * (uint64_t)(Ep * (Ep + 1) / 2)), 128, 0, st>>>(P);
+        const size_t per = (size_t)(4 * Ep + 3) * L * sizeof(double2);
+        int G = std::max(1, std::min(256 / (2 * Ep + NEc), (int)((100 << 10) / per)));
+        if ((size_t)G * per <= (size_t)(220 << 10)) {
+          P.G = G;
+          ++lhaf::g_launches;
+          tree_bc_k<<<(unsigned)((n + G - 1) / G), 128, (size_t)G * per, st>>>(P);
+        } else {
+          lhaf::g_launches += 2;
+          tree_tmat_g<<<blocks_for(n * Ep), 128, 0, st>>>(P);
+          tree_update_g<<<blocks_for(n * (uint64_t)NEc), 128, 0, st>>>(P);
+        }
       }
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
@@ -569,6 +926,7 @@ struct Runner {
     for (uint64_t p = p0; p < p1; p += cap[0]) {
       const uint64_t n = std::min(cap[0], p1 - p);
       const int NE = E[0] * (E[0] + 1) / 2;
+      ++lhaf::g_launches;
       tree_root_k<<<blocks_for(n * NE), 128, 0, st>>>(J, g.d_pats, p, n, w.lv[0], L, E[0], g.bord);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
@@ -648,6 +1006,12 @@ double tree_cmacs_per_term(const TreeGroup &g) {
 
 cudaError_t tree_run(const JobDev &J, TreeGroup &g, TreeWork &w, uint64_t ub, uint64_t ue, cudaStream_t st) {
   if (ue <= ub) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tree::tree_bc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 << 10);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   tree::Runner R{J, g, w, st, ub, ue, g.n + 1, g.H, {}, {}, {}, {}, {}, {}};
   const int H = g.H, L = g.n + 1;
   R.E.resize(H); R.b.resize(H); R.dmin.resize(H); R.eta.resize(H); R.cap.resize(H); R.Pk.resize(H);

@@ -798,6 +798,7 @@ struct Inst {
     if (grid > units) grid = units;
     e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
+    ++lhaf::g_launches;
     kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw);
     return cudaGetLastError();
   }
@@ -819,6 +820,7 @@ struct Inst {
     if (grid > units) grid = units;
     e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
+    ++lhaf::g_launches;
     kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw);
     return cudaGetLastError();
   }
@@ -831,6 +833,7 @@ struct Inst {
     if (e != cudaSuccess) return e;
     int grid = (nt + TEAMS - 1) / TEAMS;
     if (grid > 1024) grid = 1024;
+    ++lhaf::g_launches;
     kern<<<grid, THREADS, smem, s>>>(job, t, nt, g_out, tw);
     return cudaGetLastError();
   }

@@ -768,6 +768,7 @@ struct Inst {
     if (grid > units) grid = units;
     e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
+    ++lhaf::g_launches;
     kern<<<(unsigned)grid, THREADS, smem, s>>>(job, ubeg, uend, tw);
     return cudaGetLastError();
   }
@@ -780,6 +781,7 @@ struct Inst {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int grid = nt < 1184 ? nt : 1184;
+    ++lhaf::g_launches;
     kern<<<grid, THREADS, smem, s>>>(job, t, nt, g_out, tw);
     return cudaGetLastError();
   }
@@ -841,6 +843,7 @@ cudaError_t launch_sieve_mg_v5(const JobDev &job, int e_max, int g_max, int n_ma
   if (grid > uend - ubeg) grid = uend - ubeg;
   e = cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
+  ++lhaf::g_launches;
   kern<<<(unsigned)grid, 32 * NW, smem, s>>>(job, ubeg, uend, tw);
   return cudaGetLastError();
 }

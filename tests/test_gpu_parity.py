@@ -112,12 +112,39 @@ def test_batch_mixed_shapes(lib, orc):
         assert rel(v, ref) <= 1e-10, (p, v, ref)
 
 
+def tree_order(pairs, eta):
+    """The evaluation order of the tree variant, restated from its rule: the
+    pair eliminated first (last in the list) is the one with the smallest odd eta; the others
+    by descending eta (stable).  Integer bookkeeping only."""
+    H = len(eta)
+    odd = [h for h in range(H) if eta[h] % 2]
+    root = min(odd, key=lambda h: (eta[h], h)) if odd else None
+    rest = sorted([h for h in range(H) if h != root], key=lambda h: -eta[h])
+    order = rest + ([root] if root is not None else [])
+    return [pairs[h] for h in order], [eta[h] for h in order]
+
+
+def job_order(lib, orc, job, reps, mixed):
+    """The job's pair order, checked against the oracle's matching (same pairs, permuted by
+    the rule above when the job runs the tree), and the oracle's (C, v) in that order."""
+    reps_o = np.concatenate([reps, reps]) if mixed else reps
+    pairs, eta, left = orc.matched_reps(reps_o)
+    if left is not None:
+        pairs, eta = pairs + [(left, -1)], eta + [1]
+    if job.info.kernel == 6:
+        pairs, eta = tree_order(pairs, eta)
+    jp = job.plan(0)
+    assert jp.pairs() == [(int(p), int(q)) for p, q in pairs] and jp.etas() == eta
+    return pairs, eta, jp
+
+
 @pytest.mark.parametrize("which", ["cfg4_d60", "cfg5_d48", "cfg2_d24"])
 def test_per_term_parity(lib, orc, which):
     # P14: g(t) on 1024 seeded sampled t at d = 60 (cfg4), 48 (cfg5, greedy matching of the
     # doubled pattern, C11b) and 24 (a cfg2 pattern) against the oracle's explicit-power term
-    # (long double).  Reported: median and max of |g_gpu - g_ref| / |g_ref| per term and of
-    # |g_gpu - g_ref| / max_t |g_ref|; asserted: the latter <= 1e-10 for every sampled t.
+    # (long double), t decoded in the job's pair order (the per-term kernel, v3).  Reported:
+    # median and max of |g_gpu - g_ref| / |g_ref| per term and of |g_gpu - g_ref| / max_t
+    # |g_ref|; asserted: the latter <= 1e-10 for every sampled t.
     if which == "cfg4_d60":
         cfg, mixed = G.config(4), False
     elif which == "cfg5_d48":
@@ -125,13 +152,12 @@ def test_per_term_parity(lib, orc, which):
     else:
         c2 = G.config(2)
         cfg, mixed = dict(A=c2["A"], gamma=c2["gamma"], reps=c2["reps_batch"][0]), False
-    reps_o = np.concatenate([cfg["reps"], cfg["reps"]]) if mixed else cfg["reps"]
-    C, v, eta, n = orc.reduced_system(cfg["A"], cfg["gamma"], reps_o, mixed=False)
-    info = lib.lhaf_plan(cfg["reps"], mixed=mixed)
-    assert info.etas() == eta and info.n == n
     job = lib.Job(cfg["A"], cfg["gamma"], cfg["reps"], mixed=mixed)
+    pairs, eta, jp = job_order(lib, orc, job, cfg["reps"], mixed)
+    C, v = orc.reduced_from_pairs(cfg["A"], cfg["gamma"], pairs)
+    n = sum(eta)
     rng = G.rng_for(99)
-    ts = rng.integers(0, info.T_eval, 1024, dtype=np.uint64)
+    ts = rng.integers(0, jp.T_eval, 1024, dtype=np.uint64)
     gg = job.terms_g(ts)
     job.close()
     W = np.array([orc.decode(int(t), eta)[1] for t in ts], np.int32)
@@ -398,29 +424,30 @@ def test_et_inclusion_exclusion_vs_oracle(lib, orc):
 
 @pytest.mark.parametrize("c,last", [(4, True), (4, False), (5, True), (5, False)])
 def test_full_size_sieve_unit_vs_oracle(lib, orc, c, last):
-    # The bench's own launch (the sieve kernel instance, work-unit layout and finalize) at the
-    # BASELINE config's full size, on one work unit: 2^{1-n} times the oracle's long-double
-    # sum of the same term range (halving C6).  Tolerance: per-term accuracy (1e-13
-    # relative) times sum |term| of the unit.  cfg5 (mixed) is planned by the
-    # greedy matching of the doubled pattern (C11b), so the oracle sums the doubled pattern;
-    # with the natural pairing its terms are ill-conditioned in FP64.
+    # The bench's own launch (the default path: the tree's level kernels, work-unit layout and
+    # finalize) at the BASELINE config's full size, on one work unit: 2^{1-n} times the
+    # oracle's long-double sum of the same terms (halving C6).  A unit is a contiguous
+    # range of T_eval / units terms in the job's pair order (for the tree: one subtree, the
+    # top digits fixed).  Tolerance: 1e-12 of the unit's sum |term|.  cfg5 (mixed) is planned
+    # by the greedy matching of the doubled pattern (C11b).
     cfg = G.config(c)
-    info = lib.lhaf_plan(cfg["reps"], mixed=cfg["mixed"])
     job = lib.Job(cfg["A"], cfg["gamma"], cfg["reps"], mixed=cfg["mixed"])
+    pairs, eta, jp = job_order(lib, orc, job, cfg["reps"], cfg["mixed"])
     U = job.units
-    chunk = max(64, -(-info.T_eval // 131072))
-    assert U == -(-info.T_eval // chunk)
+    chunk = jp.T_eval // U
+    assert chunk * U == jp.T_eval
     u = U - 1 if last else 0
-    t0, t1 = u * chunk, min(info.T_eval, (u + 1) * chunk)
+    t0, t1 = u * chunk, (u + 1) * chunk
     job.reset()
     job.run(u, u + 1)
     got = job.finalize()[0]
     sabs = job.abs_sum()[0]
     job.close()
-    reps_o = np.concatenate([cfg["reps"], cfg["reps"]]) if cfg["mixed"] else cfg["reps"]
-    s, cnt = orc.fds_range(cfg["A"], cfg["gamma"], reps_o, t0, t1, mixed=False)
-    assert cnt == t1 - t0
-    want = s * 2.0 ** (1 - info.n)
+    C, v = orc.reduced_from_pairs(cfg["A"], cfg["gamma"], pairs)
+    n = sum(eta)
+    s, oabs = orc.fds_sum(C, v, eta, n, t0, t1)
+    want = s * 2.0 ** (1 - n)
+    assert abs(sabs - oabs * 2.0 ** (1 - n)) <= 1e-10 * sabs
     assert abs(got - want) <= 1e-12 * sabs, (c, u, got, want, sabs)
 
 

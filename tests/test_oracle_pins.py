@@ -349,3 +349,30 @@ def test_fds_terms_equals_fds_term(orc):
     got = orc.fds_terms(C, v, W, n)
     for t in range(T):
         assert got[t] == orc.fds_term(C, v, W[t], n)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fds_sum_permuted_order_pinned(orc, seed):
+    # fds_sum over the whole range of a PERMUTED pair order (the tree variant's order) equals
+    # brute force (any order of the sieve's pairs gives the same sum), and its
+    # halves add up (the term ranges the GPU's work units cover)
+    rng = G.rng_for(4300 + seed)
+    k = int(rng.integers(3, 7))
+    A = G.random_symmetric(k, rng)
+    g = G.complex_gaussian(k, 0.8, rng)
+    reps = G.random_pattern(k, int(rng.integers(2, 12)), rng)
+    pairs, eta, left = orc.matched_reps(reps)
+    if left is not None:
+        pairs, eta = pairs + [(left, -1)], eta + [1]
+    perm = rng.permutation(len(pairs))
+    pairs, eta = [pairs[i] for i in perm], [eta[i] for i in perm]
+    C, v = orc.reduced_from_pairs(A, g, pairs)
+    n = sum(eta)
+    T = int(np.prod([e + 1 for e in eta]))
+    s, sabs = orc.fds_sum(C, v, eta, n, 0, T)
+    brute = orc.lhaf(A, g, reps, method="brute")
+    assert abs(s * 2.0 ** -n - brute) <= 1e-11 * max(abs(brute), 1e-3)
+    cut = T // 3
+    s1, _ = orc.fds_sum(C, v, eta, n, 0, cut)
+    s2, _ = orc.fds_sum(C, v, eta, n, cut, T)
+    assert abs(s1 + s2 - s) <= 1e-12 * max(sabs, 1e-3)
