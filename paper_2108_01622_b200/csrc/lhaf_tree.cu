@@ -57,6 +57,12 @@ struct SR {  // series view: element s at p[s * st]
 };
 __device__ __forceinline__ double2 at(const SR &r, int i) { return r.p[(int64_t)i * r.st]; }
 __device__ __forceinline__ int tri(int i, int j) { return i * (i + 1) / 2 + j; }
+// 16-byte global -> shared copies that bypass the registers (and L1)
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // acc[k] += sum_{s + q = t0 + k - sh} a[s] b[q]   (0 <= s < La, 0 <= q < Lb; k < TB)
 // The b operand streams through a TB-slot window in registers (one new value per step, slot
@@ -330,6 +336,43 @@ __device__ __forceinline__ void rdet(double2 (&A)[LM], const double2 *Kab, const
   }
 }
 
+// The three recursions of the method in one routine (one code instance per kernel):
+//   X[t] = alpha_t (gamma t P[t] + beta sum_{s=1}^{t} P[s] X[t-s]),  X[0] = x0
+//   1/P:       x0 = 1, gamma = 0, beta = -1, alpha = 1
+//   t log P_t: x0 = 0, gamma = 1, beta = -1, alpha = 1   (t l_t = t P_t - sum_s P_s (t-s) l_{t-s}, P_0 = 1)
+//   exp(phi):  x0 = 1, gamma = 0, beta = 1,  alpha = 1/t  (P = Psi, Psi_t = t phi_t)
+template <int LM>
+__device__ __forceinline__ void rrec(double2 (&X)[LM], const double2 (&P)[LM], int L, double x0, double gamma,
+                                     double beta, bool inv_t) {
+  X[0] = make_double2(x0, 0.0);
+#pragma unroll
+  for (int t = 1; t < LM; ++t) {
+    double2 x = c0();
+    if (t < L) {
+#pragma unroll
+      for (int s = 1; s <= t; ++s) x = cfma(P[s], X[t - s], x);
+      x = cscale(x, beta);
+      x.x = fma(gamma * t, P[t].x, x.x);
+      x.y = fma(gamma * t, P[t].y, x.y);
+      if (inv_t) x = cscale(x, 1.0 / t);
+    }
+    X[t] = x;
+  }
+}
+// acc[t] += sgn * sum_{s + q = t} a[s] B[q] (a streamed; runtime sign: one code instance)
+template <int LM>
+__device__ __forceinline__ void rs_op(double2 (&acc)[LM], const double2 *__restrict__ a, const double2 (&B)[LM], int L,
+                                      double sgn) {
+#pragma unroll
+  for (int s = 0; s < LM; ++s) {
+    if (s < L) {
+      const double2 av = cscale(a[s], sgn);
+#pragma unroll
+      for (int q = 0; q + s < LM; ++q) acc[q + s] = cfma(av, B[q], acc[q + s]);
+    }
+  }
+}
+
 // ================================================================ kernels
 struct TStep {  // parent depth k -> children at depth k + 1, one chunk of children
   TLevel par, ch;
@@ -426,7 +469,17 @@ __global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
 // the parent rows (u, x) and the children's Q in shared memory, T written there, then the
 // packed lower triangle of every child.  Shared layout per child: U[Ep][L] X[Ep][L] Q[3][L]
 // T1[Ep][L] T2[Ep][L].
-__global__ void __launch_bounds__(128) tree_bc_k(TStep P) {
+#ifndef LHAF_BC_THREADS
+#define LHAF_BC_THREADS 128
+#endif
+#ifndef LHAF_BC_MINB
+#define LHAF_BC_MINB 3
+#endif
+#ifndef LHAF_BC_SMEM_KB
+#define LHAF_BC_SMEM_KB 72
+#endif
+constexpr int BC_THREADS = LHAF_BC_THREADS;
+__global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   extern __shared__ double2 sm[];
   const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1, Ep = E - 2;
   const int NEc = Ep * (Ep + 1) / 2;
@@ -442,12 +495,16 @@ __global__ void __launch_bounds__(128) tree_bc_k(TStep P) {
     const double2 *ur = Kp + (int64_t)tri(a, 0) * L, *xr = Kp + (int64_t)tri(b, 0) * L;
     const double2 *qr = P.Q + (int64_t)(g0 + g) * 3 * L;
     double2 *base = sm + (int64_t)g * per;
-    for (int t = tid; t < Ep * L; t += 128) { base[t] = ur[t]; base[Ep * L + t] = xr[t]; }
-    for (int t = tid; t < 3 * L; t += 128) base[2 * Ep * L + t] = qr[t];
+    for (int t = tid; t < Ep * L; t += BC_THREADS) {
+      cp_async16(base + t, ur + t);
+      cp_async16(base + Ep * L + t, xr + t);
+    }
+    for (int t = tid; t < 3 * L; t += BC_THREADS) cp_async16(base + 2 * Ep * L + t, qr + t);
   }
+  cp_async_wait_all();
   __syncthreads();
   const int Lo = L - 1;
-  for (int task = tid; task < G * 2 * Ep; task += 128) {
+  for (int task = tid; task < G * 2 * Ep; task += BC_THREADS) {
     const int g = task / (2 * Ep), r = task - g * 2 * Ep, j = r >> 1, which = r & 1;
     double2 *base = sm + (int64_t)g * per;
     const double2 *U = base, *X = base + Ep * L, *Qs = base + 2 * Ep * L;
@@ -466,7 +523,7 @@ __global__ void __launch_bounds__(128) tree_bc_k(TStep P) {
     }
   }
   __syncthreads();
-  for (int task = tid; task < G * NEc; task += 128) {
+  for (int task = tid; task < G * NEc; task += BC_THREADS) {
     const int g = task / NEc, e = task - g * NEc;
     int ii = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
     while (tri(ii + 1, 0) <= e) ++ii;
@@ -560,6 +617,7 @@ struct TLeaf {
 // The last pair of every node, both (all) digits; the node-level products shared by the leaves:
 // Delta = K_ab^2 - K_aa K_bb, and with the border P = u (K_bb u - K_ab x) + x (K_aa x - K_ab u)
 // and N0 = u x, so that the leaf's border entry is K'_00 = K_00 + lam R_w (lam w^2 P + 2 w N0).
+// Scratch per node (HBM, L1-resident while the thread works): S0 Delta, S1 P, S2 N0, S3.
 template <int LM>
 __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
@@ -568,89 +626,80 @@ __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
   const double2 *Kp = P.par.K + (int64_t)i * NE * L;
   const double2 *Kaa = Kp + (int64_t)tri(a, a) * L, *Kbb = Kp + (int64_t)tri(b, b) * L,
                 *Kab = Kp + (int64_t)tri(b, a) * L;
+  const double2 *u = Kp + (int64_t)tri(a, 0) * L, *x = Kp + (int64_t)tri(b, 0) * L;
   const double2 *lc = P.par.logc + (int64_t)i * L;
   double2 *S0 = P.S + (int64_t)i * 4 * L, *S1 = S0 + L, *S2 = S1 + L, *S3 = S2 + L;
   double2 A[LM], B[LM];
-  // Delta -> S0
-  rload(A, Kab, L);
-  rz(B);
-  rr_acc(B, A, A, L);
-  rload(A, Kaa, L);
-  rs_acc<LM, 0, true>(B, Kbb, A, L);
-  rstore(S0, B, L);
-  const double2 *u = nullptr, *x = nullptr, *K00 = nullptr;
-  if (P.bord) {
-    u = Kp + (int64_t)tri(a, 0) * L;
-    x = Kp + (int64_t)tri(b, 0) * L;
-    K00 = Kp;
-    rload(A, u, L);                      // P1 = Kbb u - Kab x -> S1
-    rz(B);
-    rs_acc<LM, 0, false>(B, Kbb, A, L);
-    rload(A, x, L);
-    rs_acc<LM, 0, true>(B, Kab, A, L);
-    rstore(S1, B, L);
-    rz(B);                               // P2 = Kaa x - Kab u -> S2
-    rs_acc<LM, 0, false>(B, Kaa, A, L);
-    rload(A, u, L);
-    rs_acc<LM, 0, true>(B, Kab, A, L);
-    rstore(S2, B, L);
-    rz(B);                               // P = u P1 + x P2 -> S1
-    rs_acc<LM, 0, false>(B, S1, A, L);
-    rload(A, x, L);
-    rs_acc<LM, 0, false>(B, S2, A, L);
-    rstore(S1, B, L);
-    rz(B);                               // N0 = u x -> S2
-    rs_acc<LM, 0, false>(B, u, A, L);
-    rstore(S2, B, L);
+  rload(B, Kab, L);
+  rz(A);
+  rr_acc(A, B, B, L);                       // A = Kab^2
+  // node-level ops on (acc A, operand B):
+  //  0: B=Kaa  A -= Kbb B -> S0 (Delta)       [no border: stop here]
+  //  1: B=u    A  = Kbb B                      2: B=x  A -= Kab B -> S1 (P1)
+  //  3:        A  = Kaa B                      4: B=u  A -= Kab B -> S2 (P2)
+  //  5:        A  = S1 B                       6: B=x  A += S2 B -> S1 (P)
+  //  7:        A  = u B -> S2 (N0)
+  const int nops = P.bord ? 8 : 1;
+#pragma unroll 1
+  for (int op = 0; op < nops; ++op) {
+    const double2 *ld = (op == 0) ? Kaa : (op == 1 || op == 4) ? u : (op == 2 || op == 6) ? x : nullptr;
+    if (ld) rload(B, ld, L);
+    if (op == 1 || op == 3 || op == 5 || op == 7) rz(A);
+    const double2 *src = (op == 0 || op == 1) ? Kbb : (op == 2 || op == 4) ? Kab : (op == 3) ? Kaa
+                       : (op == 5) ? S1 : (op == 6) ? S2 : u;
+    const double sg = (op == 0 || op == 2 || op == 4) ? -1.0 : 1.0;
+    rs_op(A, src, B, L, sg);
+    double2 *st = (op == 0) ? S0 : (op == 2 || op == 6) ? S1 : (op == 4 || op == 7) ? S2 : nullptr;
+    if (st) rstore(st, A, L);
   }
   const double coef = P.par.coef[i];
   double2 vsum = c0();
   double asum = 0.0;
+#pragma unroll 1
   for (int d = 0; d < P.b; ++d) {
     const int kh = P.dmin + d, w = P.eta - 2 * kh;
     const double wd = (double)w, w2 = wd * wd;
-    rdet(A, Kab, S0, w, L);              // A = D_w
-    rrecip(B, A, L);                     // B = R_w
-    rtlog_inplace(A, B, L);              // A = t log D_w
-    if (P.bord) {
-      rstore(S3, A, L);
-      // A = R_w (lam w^2 P + 2 w N0): stream N_w[s] = w^2 P[s-1] + 2 w N0[s]
-      rz(A);
+    // phases sharing one recursion instance: 0: R = 1/D; 1: t log D; 2: exp(phi)
+#pragma unroll 1
+    for (int ph = 0; ph < 3; ++ph) {
+      if (ph < 2) rdet(A, Kab, S0, w, L);   // A = D_w
+      rrec(B, A, L, ph == 1 ? 0.0 : 1.0, ph == 1 ? 1.0 : 0.0, ph == 2 ? 1.0 : -1.0, ph == 2);
+      if (ph == 0) {
+        if (P.bord) {
+          // S3 = N_w = lam w^2 P + 2 w N0;  A = R_w N_w;  S3 = A (lam M enters K'_00)
 #pragma unroll
-      for (int s = 0; s < LM; ++s) {
-        if (s < L) {
-          double2 nv = cscale(S2[s], 2.0 * wd);
-          if (s >= 1) { const double2 pv = S1[s - 1]; nv.x += w2 * pv.x; nv.y += w2 * pv.y; }
-#pragma unroll
-          for (int q = 0; q + s < LM; ++q) A[q + s] = cfma(nv, B[q], A[q + s]);
+          for (int t = 0; t < LM; ++t)
+            if (t < L) {
+              double2 nv = cscale(S2[t], 2.0 * wd);
+              if (t >= 1) { const double2 pv = S1[t - 1]; nv.x += w2 * pv.x; nv.y += w2 * pv.y; }
+              S3[t] = nv;
+            }
+          rz(A);
+          rs_op(A, S3, B, L, 1.0);
+          rstore(S3, A, L);
         }
-      }
-      // B = Psi_t = t phi_t, phi = 1/2 (K00 + lam M - log c - log D)
+      } else if (ph == 1) {
+        // A = Psi_t = t phi_t, phi = 1/2 (K00 + lam M - log c - log D)   (B = t log D)
 #pragma unroll
-      for (int t = 0; t < LM; ++t) {
-        double2 ps = c0();
-        if (t >= 1 && t < L) {
-          const double2 k0 = K00[t], l0 = lc[t], tl = S3[t], m = A[t - 1];
-          ps = make_double2(0.5 * (t * (k0.x + m.x - l0.x) - tl.x), 0.5 * (t * (k0.y + m.y - l0.y) - tl.y));
+        for (int t = 0; t < LM; ++t) {
+          double2 ps = c0();
+          if (t >= 1 && t < L) {
+            const double2 l0 = lc[t], tl = B[t];
+            if (P.bord) {
+              const double2 k0 = Kp[t], m = S3[t - 1];
+              ps = make_double2(0.5 * (t * (k0.x + m.x - l0.x) - tl.x), 0.5 * (t * (k0.y + m.y - l0.y) - tl.y));
+            } else {
+              ps = make_double2(-0.5 * (t * l0.x + tl.x), -0.5 * (t * l0.y + tl.y));
+            }
+          }
+          A[t] = ps;
         }
-        B[t] = ps;
-      }
-    } else {
-#pragma unroll
-      for (int t = 0; t < LM; ++t) {
-        double2 ps = c0();
-        if (t >= 1 && t < L) {
-          const double2 l0 = lc[t];
-          ps = make_double2(-0.5 * (t * l0.x + A[t].x), -0.5 * (t * l0.y + A[t].y));
-        }
-        B[t] = ps;
       }
     }
-    rexp(A, B, L);
     double2 g = c0();
 #pragma unroll
     for (int t = 0; t < LM; ++t)
-      if (t == L - 1) g = A[t];
+      if (t == L - 1) g = B[t];
     const double f = coef * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
     vsum.x = fma(f, g.x, vsum.x);
     vsum.y = fma(f, g.y, vsum.y);
@@ -901,11 +950,11 @@ struct Runner {
       else tree_pivot_g<<<blocks_for(n), 128, 0, st>>>(P);
       if (Ep > 0) {
         const size_t per = (size_t)(4 * Ep + 3) * L * sizeof(double2);
-        int G = std::max(1, std::min(256 / (2 * Ep + NEc), (int)((100 << 10) / per)));
+        int G = std::max(1, std::min(2 * BC_THREADS / (2 * Ep + NEc), (int)((LHAF_BC_SMEM_KB << 10) / per)));
         if ((size_t)G * per <= (size_t)(220 << 10)) {
           P.G = G;
           ++lhaf::g_launches;
-          tree_bc_k<<<(unsigned)((n + G - 1) / G), 128, (size_t)G * per, st>>>(P);
+          tree_bc_k<<<(unsigned)((n + G - 1) / G), BC_THREADS, (size_t)G * per, st>>>(P);
         } else {
           lhaf::g_launches += 2;
           tree_tmat_g<<<blocks_for(n * Ep), 128, 0, st>>>(P);
