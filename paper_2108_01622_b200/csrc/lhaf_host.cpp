@@ -405,7 +405,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   bool use_tree = g_ctx.variant == 6 || (g_ctx.variant == 0 && g_ctx.precision == 0);
   if (plans_in)
     for (const Plan &Pm : *plans_in)
-      if (Pm.et || Pm.eta_b >= 0 || Pm.mg > 0) use_tree = false;
+      if (Pm.eta_b >= 0 || Pm.mg > 0) use_tree = false;
 
   lhaf_job *j = new lhaf_job();
   j->batch = batch;
@@ -440,7 +440,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       s = make_plan(reps + (size_t)b * k, k, mixed, P);
     }
     bool full = false;
-    if (s == LHAF_OK && use_tree && P.H > 0 && !tree_order(P)) {
+    if (s == LHAF_OK && use_tree && P.H > 0 && !tree_order(P) && !P.et) {
       full = true;       // every eta even: no halving, the whole range [0, T)
       P.T_eval = P.T;
     }
@@ -523,7 +523,9 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     for (int b = 0; b < batch; ++b) {
       const PatDesc &D = j->descs[b];
       if (D.H == 0 || D.T_eval == 0) continue;
-      std::vector<int> key = {D.H, D.n, (D.flags & FLAG_LOOP) ? 1 : 0, (D.flags & FLAG_FULL) ? 0 : 1};
+      const bool et = (D.flags & FLAG_ET) != 0;
+      std::vector<int> key = {D.H, D.n, (D.flags & FLAG_LOOP) ? 1 : 0, (D.flags & (FLAG_FULL | FLAG_ET)) ? 0 : 1,
+                              et ? 1 : 0};
       for (int h = 0; h < D.H; ++h) key.push_back(ipool[D.eta_off + h]);
       size_t gi = 0;
       while (gi < keys.size() && keys[gi] != key) ++gi;
@@ -531,7 +533,8 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
         keys.push_back(key);
         TreeGroup g;
         g.H = D.H; g.n = D.n; g.bord = key[2]; g.halve = key[3];
-        g.eta.assign(key.begin() + 4, key.end());
+        g.wmul = key[4] ? 1 : 2;  // inclusion/exclusion: w = eta - k; sieve: eta - 2k
+        g.eta.assign(key.begin() + 5, key.end());
         j->groups.push_back(g);
       }
       j->groups[gi].pats.push_back(b);

@@ -122,6 +122,7 @@ struct TLevel {   // the nodes of one depth: K[(s * NE + e) * cap + node], logc[
 }  // namespace tree
 struct TreeGroup {            // patterns that share one tree shape
   int H = 0, n = 0, bord = 0, halve = 1, k_u = 0, npat = 0;
+  int wmul = 2;               // digit k -> weight eta - wmul k (2: the sieve; 1: inclusion/exclusion)
   std::vector<int> eta;       // tree order: pair H-1 is eliminated first (depth 0)
   std::vector<int32_t> pats;  // job pattern indices, in unit order
   int32_t *d_pats = nullptr;

@@ -379,7 +379,7 @@ struct TStep {  // parent depth k -> children at depth k + 1, one chunk of child
   uint64_t pbase;  // global index of the parent buffer's slot 0
   uint64_t c0;     // global index of the first child (slot 0 of the child buffer)
   uint64_t nc;     // children in the chunk
-  int L, E, b, dmin, eta;
+  int L, E, b, dmin, eta, wmul;
   double2 *Q;      // [nc][3][L]: q11, q12, q22 of every child
   double2 *S;      // fallback scratch
   double2 *T;      // fallback T: [nc][2][E-2][L]
@@ -390,10 +390,30 @@ __device__ __forceinline__ void child_of(const TStep &P, uint64_t i, uint64_t &p
   const uint64_t c = P.c0 + i, pg = c / P.b;
   ps = pg - P.pbase;
   kh = P.dmin + (int)(c - pg * P.b);
-  w = P.eta - 2 * kh;
+  w = P.eta - P.wmul * kh;
 }
 
-// D = 1 - 2 w lam K_ab + w^2 lam^2 (K_ab^2 - K_aa K_bb), R = 1/D, t log D_t, Q; series in registers.
+// Delta = K_ab^2 - K_aa K_bb of every parent of the chunk (shared by its children: the weight
+// enters only D = 1 - 2 w lam K_ab + w^2 lam^2 Delta), into P.S[(parent - first parent) * L]
+template <int LM>
+__global__ void __launch_bounds__(128) tree_delta_r(TStep P, uint64_t np) {
+  const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
+  if (i >= np) return;
+  const uint64_t ps = P.c0 / P.b + i - P.pbase;
+  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
+  const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
+  double2 A[LM], B[LM];
+  rload(B, Kp + (int64_t)tri(b, a) * L, L);
+  rz(A);
+  rr_acc(A, B, B, L);
+  rload(B, Kp + (int64_t)tri(a, a) * L, L);
+  rs_op(A, Kp + (int64_t)tri(b, b) * L, B, L, -1.0);
+  rstore(P.S + (int64_t)i * L, A, L);
+}
+
+// Per child: D_w, R = 1/D_w, t log D_w (child log c), Q.  Series in two register arrays; each
+// triangular routine appears once (rolled loops over the phases that share it: the unrolled
+// bodies are large, and the instruction cache limited the first version).
 template <int LM>
 __global__ void __launch_bounds__(128) tree_pivot_r(TStep P) {
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
@@ -404,51 +424,42 @@ __global__ void __launch_bounds__(128) tree_pivot_r(TStep P) {
   const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
   const double2 *Kaa = Kp + (int64_t)tri(a, a) * L, *Kbb = Kp + (int64_t)tri(b, b) * L,
                 *Kab = Kp + (int64_t)tri(b, a) * L;
+  const double2 *Dl = P.S + (int64_t)((P.c0 + i) / P.b - P.c0 / P.b) * L;
   const double2 *lp = P.par.logc + (int64_t)ps * L;
   double2 *lc = P.ch.logc + (int64_t)i * L;
   double2 *Q = P.Q + (int64_t)i * 3 * L;
   const double wd = (double)w, w2 = wd * wd;
-  double2 A[LM], B[LM];
+  P.ch.coef[i] = P.par.coef[ps] * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
   if (w == 0) {  // deleted pair: D = 1, Q = 0
     for (int t = 0; t < L; ++t) { lc[t] = lp[t]; Q[t] = Q[L + t] = Q[2 * L + t] = c0(); }
-  } else {
-    rload(A, Kab, L);
-    rz(B);
-    rr_acc(B, A, A, L);                 // Kab^2
-    rload(A, Kaa, L);
-    rs_acc<LM, 0, true>(B, Kbb, A, L);  // - Kaa Kbb
-    // rdet streams Delta from memory; keep it in registers instead: A = D from B
-#pragma unroll
-    for (int t = LM - 1; t >= 0; --t) {
-      double2 d = (t == 0) ? c1() : c0();
-      if (t < L) {
-        if (t >= 1) { const double2 k = Kab[t - 1]; d.x -= 2.0 * wd * k.x; d.y -= 2.0 * wd * k.y; }
-        if (t >= 2) { d.x += w2 * B[t - 2].x; d.y += w2 * B[t - 2].y; }
-      }
-      A[t] = d;
-    }
-    rrecip(B, A, L);                    // B = R
-    rtlog_inplace(A, B, L);             // A = t log D_t
-#pragma unroll
-    for (int t = 0; t < LM; ++t)
-      if (t < L) lc[t] = t ? cadd(lp[t], cscale(A[t], 1.0 / t)) : lp[t];
-    rz(A);
-    rs_acc<LM, 1, false>(A, Kbb, B, L);
-#pragma unroll
-    for (int t = 0; t < LM; ++t)
-      if (t < L) Q[t] = cscale(A[t], w2);                      // q11 = lam w^2 Kbb R
-    rz(A);
-    rs_acc<LM, 1, false>(A, Kaa, B, L);
-#pragma unroll
-    for (int t = 0; t < LM; ++t)
-      if (t < L) Q[2 * L + t] = cscale(A[t], w2);              // q22 = lam w^2 Kaa R
-    rz(A);
-    rs_acc<LM, 1, false>(A, Kab, B, L);
-#pragma unroll
-    for (int t = 0; t < LM; ++t)
-      if (t < L) Q[L + t] = make_double2(wd * B[t].x - w2 * A[t].x, wd * B[t].y - w2 * A[t].y);  // q12
+    return;
   }
-  P.ch.coef[i] = P.par.coef[ps] * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
+  double2 A[LM], B[LM];
+#pragma unroll 1
+  for (int ph = 0; ph < 2; ++ph) {
+    rdet(A, Kab, Dl, w, L);                                   // A = D_w
+    rrec(B, A, L, ph ? 0.0 : 1.0, ph ? 1.0 : 0.0, -1.0, false);  // B = 1/D (ph 0), t log D (ph 1)
+    if (ph == 0) {
+#pragma unroll 1
+      for (int qi = 0; qi < 3; ++qi) {                        // lam K R for K = Kbb, Kaa, Kab
+        rz(A);
+        rs_op(A, qi == 0 ? Kbb : qi == 1 ? Kaa : Kab, B, L, 1.0);
+#pragma unroll
+        for (int t = 0; t < LM; ++t) {
+          if (t < L) {
+            const double2 m = t ? A[t - 1] : c0();
+            if (qi == 0) Q[t] = cscale(m, w2);                                           // q11
+            else if (qi == 1) Q[2 * L + t] = cscale(m, w2);                              // q22
+            else Q[L + t] = make_double2(wd * B[t].x - w2 * m.x, wd * B[t].y - w2 * m.y);  // q12
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < LM; ++t)
+        if (t < L) lc[t] = t ? cadd(lp[t], cscale(B[t], 1.0 / t)) : lp[t];
+    }
+  }
 }
 
 // generic pivot (any L): the blocked series routines above with per-child scratch in HBM
@@ -504,14 +515,26 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   cp_async_wait_all();
   __syncthreads();
   const int Lo = L - 1;
-  for (int task = tid; task < G * 2 * Ep; task += BC_THREADS) {
-    const int g = task / (2 * Ep), r = task - g * 2 * Ep, j = r >> 1, which = r & 1;
+  // tasks are split by output blocks, paired (p, nb - 1 - p) so that every task does about the
+  // same work (the products are triangular): PB parts per series
+  const int nbB = (Lo + TB - 1) / TB, PB = (nbB + 1) / 2;
+  for (int task = tid; task < G * 2 * Ep * PB; task += BC_THREADS) {
+    const int part = task % PB, tk = task / PB;
+    const int g = tk / (2 * Ep), r = tk - g * 2 * Ep, j = r >> 1, which = r & 1;
+    {
+      uint64_t ps; int kh, w;
+      child_of(P, g0 + g, ps, kh, w);
+      if (w == 0) continue;  // deleted pair: the child is the parent's leading block
+    }
     double2 *base = sm + (int64_t)g * per;
     const double2 *U = base, *X = base + Ep * L, *Qs = base + 2 * Ep * L;
     double2 *T = base + (2 * Ep + 3) * L + (int64_t)which * Ep * L + (int64_t)j * L;
     // T1 = q11 u + q12 x ; T2 = q12 u + q22 x
     const SR qa{Qs + (which ? L : 0), 1}, qb{Qs + (which ? 2 * L : L), 1};
-    for (int t0 = 0; t0 < Lo; t0 += TB) {
+    for (int bi = 0; bi < 2; ++bi) {
+      const int blk = bi ? nbB - 1 - part : part;
+      if (bi && blk == part) break;
+      const int t0 = blk * TB;
       double2 acc[TB];
 #pragma unroll
       for (int k = 0; k < TB; ++k) acc[k] = c0();
@@ -523,8 +546,10 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
     }
   }
   __syncthreads();
-  for (int task = tid; task < G * NEc; task += BC_THREADS) {
-    const int g = task / NEc, e = task - g * NEc;
+  const int nbC = (L + TB - 1) / TB, PC = (nbC + 1) / 2;
+  for (int task = tid; task < G * NEc * PC; task += BC_THREADS) {
+    const int part = task % PC, tk = task / PC;
+    const int g = tk / NEc, e = tk - g * NEc;
     int ii = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
     while (tri(ii + 1, 0) <= e) ++ii;
     while (tri(ii, 0) > e) --ii;
@@ -535,7 +560,14 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
     const double2 *U = base, *X = base + Ep * L, *T1 = base + (2 * Ep + 3) * L, *T2 = T1 + Ep * L;
     const double2 *K = P.par.K + ((int64_t)ps * NE + e) * L;
     double2 *out = P.ch.K + ((int64_t)(g0 + g) * NEc + e) * L;
-    for (int t0 = 0; t0 < L; t0 += TB) {
+    for (int bi = 0; bi < 2; ++bi) {
+      const int blk = bi ? nbC - 1 - part : part;
+      if (bi && blk == part) break;
+      const int t0 = blk * TB;
+      if (w == 0) {
+        for (int t = t0; t < t0 + TB && t < L; ++t) out[t] = K[t];
+        continue;
+      }
       double2 acc[TB];
 #pragma unroll
       for (int k = 0; k < TB; ++k) acc[k] = (t0 + k < L) ? K[t0 + k] : c0();
@@ -608,7 +640,7 @@ __global__ void __launch_bounds__(128) tree_update_g(TStep P) {
 struct TLeaf {
   TLevel par;      // nodes at depth H-1 (one pair left, plus the border)
   uint64_t np;     // nodes in the chunk
-  int L, E, bord, b, dmin, eta;
+  int L, E, bord, b, dmin, eta, wmul;
   double2 *S;      // scratch [np][9][L]
   double2 *val;    // [np]: sum over the node's leaves of sign * prod C * g
   double *absv;    // [np]: the same sum of |.|
@@ -657,7 +689,7 @@ __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
   double asum = 0.0;
 #pragma unroll 1
   for (int d = 0; d < P.b; ++d) {
-    const int kh = P.dmin + d, w = P.eta - 2 * kh;
+    const int kh = P.dmin + d, w = P.eta - P.wmul * kh;
     const double wd = (double)w, w2 = wd * wd;
     // phases sharing one recursion instance: 0: R = 1/D; 1: t log D; 2: exp(phi)
 #pragma unroll 1
@@ -723,7 +755,7 @@ __global__ void __launch_bounds__(128) tree_leaf_g(TLeaf P) {
   double2 vsum = c0();
   double asum = 0.0;
   for (int d = 0; d < P.b; ++d) {
-    const int kh = P.dmin + d, w = P.eta - 2 * kh;
+    const int kh = P.dmin + d, w = P.eta - P.wmul * kh;
     pivot(Kaa, Kbb, Kab, L, w, S, P.bord ? Qo : nullptr, 1, logc, nullptr, 0, Psi, nullptr);
     if (P.bord) {
       const SR u{Kp + (int64_t)tri(a, 0) * L, 1}, x{Kp + (int64_t)tri(b, 0) * L, 1};
@@ -899,7 +931,7 @@ struct Runner {
     TLeaf P;
     P.par = w.lv[k];
     P.np = cnt;
-    P.L = L; P.E = E[k]; P.bord = g.bord; P.b = b[k]; P.dmin = dmin[k]; P.eta = eta[k];
+    P.L = L; P.E = E[k]; P.bord = g.bord; P.b = b[k]; P.dmin = dmin[k]; P.eta = eta[k]; P.wmul = g.wmul;
     P.S = (double2 *)w.scratch;
     P.val = (double2 *)w.val;
     P.absv = (double *)w.absv;
@@ -936,21 +968,33 @@ struct Runner {
       P.pbase = gs;
       P.c0 = c;
       P.nc = n;
-      P.L = L; P.E = E[k]; P.b = b[k]; P.dmin = dmin[k]; P.eta = eta[k];
+      P.L = L; P.E = E[k]; P.b = b[k]; P.dmin = dmin[k]; P.eta = eta[k]; P.wmul = g.wmul;
       const int Ep = E[k] - 2, NEc = Ep * (Ep + 1) / 2;
       P.Q = (double2 *)w.scratch;
       P.S = P.Q + (size_t)3 * L * n;
       P.T = P.S + (size_t)3 * L * n;
       ++lhaf::g_launches;
       const int rl = reg_limit();
-      if (L <= 16 && L <= rl) tree_pivot_r<16><<<blocks_for(n), 128, 0, st>>>(P);
-      else if (L <= 24 && L <= rl) tree_pivot_r<24><<<blocks_for(n), 128, 0, st>>>(P);
-      else if (L <= 32 && L <= rl) tree_pivot_r<32><<<blocks_for(n), 128, 0, st>>>(P);
-      else if (L <= 40 && L <= rl) tree_pivot_r<40><<<blocks_for(n), 128, 0, st>>>(P);
-      else tree_pivot_g<<<blocks_for(n), 128, 0, st>>>(P);
+      const uint64_t npar = (c + n - 1) / nb - c / nb + 1;
+      if (L <= 40 && L <= rl) ++lhaf::g_launches;
+      if (L <= 16 && L <= rl) {
+        tree_delta_r<16><<<blocks_for(npar), 128, 0, st>>>(P, npar);
+        tree_pivot_r<16><<<blocks_for(n), 128, 0, st>>>(P);
+      } else if (L <= 24 && L <= rl) {
+        tree_delta_r<24><<<blocks_for(npar), 128, 0, st>>>(P, npar);
+        tree_pivot_r<24><<<blocks_for(n), 128, 0, st>>>(P);
+      } else if (L <= 32 && L <= rl) {
+        tree_delta_r<32><<<blocks_for(npar), 128, 0, st>>>(P, npar);
+        tree_pivot_r<32><<<blocks_for(n), 128, 0, st>>>(P);
+      } else if (L <= 40 && L <= rl) {
+        tree_delta_r<40><<<blocks_for(npar), 128, 0, st>>>(P, npar);
+        tree_pivot_r<40><<<blocks_for(n), 128, 0, st>>>(P);
+      } else {
+        tree_pivot_g<<<blocks_for(n), 128, 0, st>>>(P);
+      }
       if (Ep > 0) {
         const size_t per = (size_t)(4 * Ep + 3) * L * sizeof(double2);
-        int G = std::max(1, std::min(2 * BC_THREADS / (2 * Ep + NEc), (int)((LHAF_BC_SMEM_KB << 10) / per)));
+        int G = std::max(1, std::min(2 * BC_THREADS / (2 * Ep + NEc) + 1, (int)((LHAF_BC_SMEM_KB << 10) / per)));
         if ((size_t)G * per <= (size_t)(220 << 10)) {
           P.G = G;
           ++lhaf::g_launches;

@@ -136,3 +136,23 @@ def test_tree_n28_vs_v3(lib):
     v = lib.lhaf_rpt(cfg["A"], cfg["gamma"], reps)
     lib.lhaf_set_kernel(0)
     assert rel(t, v) <= 1e-9, (t, v)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_tree_inclusion_exclusion(lib, orc, seed):
+    # lhaf_rpt_et on the tree (digit k -> weight eta - k, zero weights delete the pair, no
+    # halving, prefactor 1: P:403-415) against the oracle, and against the per-term
+    # v5 evaluation of the same inclusion/exclusion sum
+    rng = G.rng_for(7600 + seed)
+    k = int(rng.integers(2, 8))
+    A = G.random_symmetric(k, rng, 0.6)
+    g = G.complex_gaussian(k, 0.5, rng) if seed % 2 else np.zeros(k, complex)
+    reps = G.random_pattern(k, int(rng.integers(2, 15)), rng)
+    ref, T, sabs = orc.lhaf_fds(A, g, reps)
+    lib.lhaf_set_kernel(6)
+    t = lib.lhaf_rpt_et(A, g, reps)
+    lib.lhaf_set_kernel(5)
+    v = lib.lhaf_rpt_et(A, g, reps)
+    lib.lhaf_set_kernel(0)
+    check(t, ref, sabs, 1e-9)
+    assert abs(t - v) <= max(1e-9 * abs(ref), 1e-12 * sabs)

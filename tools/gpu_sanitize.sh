@@ -6,7 +6,7 @@ mkdir -p gpurun_out/sanitizer
 S=/usr/local/cuda/bin/compute-sanitizer
 : > gpurun_out/sanitizer/summary.txt
 for tool in memcheck racecheck synccheck initcheck; do
-  for c in cfg1 cfg2 d48_v3 d48_v5 cfg4_v3 cfg4_v5 precise mg cutoff et; do
+  for c in cfg1 cfg2 cfg4_tree d48_tree d48_v3 d48_v5 cfg4_v3 cfg4_v5 precise mg cutoff et; do
     log=gpurun_out/sanitizer/${tool}_${c}.log
     timeout 900 $S --tool $tool --error-exitcode 9 python tools/sanitize_case.py $c > $log 2>&1
     rc=$?

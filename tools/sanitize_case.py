@@ -1,7 +1,8 @@
 """Tiny launches of every kernel family for compute-sanitizer (racecheck / synccheck / memcheck /
 initcheck): a few 64-term work units of each instance, so that a sanitizer pass stays short.
     python tools/sanitize_case.py CASE   (cfg1 | cfg2 | d48_v3 | d48_v5 | cfg4_v3 | cfg4_v5 |
-                                          precise | mg | cutoff | et)"""
+                                          precise | mg | cutoff | et | cfg4_tree | d48_tree)
+(cfg1, cfg2 and et run the default path: the tree, variant 6)"""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -31,6 +32,10 @@ elif case == "cfg2":
     small_job(G.config(2), units=8)
 elif case in ("d48_v3", "d48_v5"):
     small_job(G.config(5), kernel=3 if case.endswith("v3") else 5)
+elif case == "cfg4_tree":
+    small_job(G.config(4), units=2, kernel=6)
+elif case == "d48_tree":
+    small_job(G.config(5), units=2, kernel=6)
 elif case in ("cfg4_v3", "cfg4_v5"):
     small_job(G.config(4), kernel=3 if case.endswith("v3") else 5)
 elif case == "precise":
