@@ -402,7 +402,7 @@ def main():
                 "flops_per_term": own_term,
                 "flops_model": ("tree (variant 6): complex MACs of the level kernels per evaluated leaf x 8"
                                 if job.info.kernel == 6 else "per-term kernel: useful FP64 flops per term"),
-                "kernels": "tree_pivot_k/tree_tmat_k/tree_update_k/tree_leaf_k/tree_reduce_k (+ tree_root_k)"
+                "kernels": "tree_delta_r/tree_pivot_r/tree_bc_k/tree_leaf_r/tree_reduce_k (+ tree_root_k)"
                            if job.info.kernel == 6 else f"sieve (variant {job.info.kernel})",
                 "survey_F_per_term": flops_term,
                 "survey_F_equivalent_tflops": surveyF,

@@ -880,12 +880,14 @@ __global__ void __launch_bounds__(128) tree_root_k(JobDev J, const int32_t *pats
 
 // ------------------------------------------------------------------ host driver
 
-static cudaError_t grow(void **p, size_t &have, size_t need) {
+// Buffers come from the device's stream-ordered pool (its release threshold is kept at the
+// maximum, lhaf_host.cpp): a new job reuses the memory of the jobs destroyed before it.
+static cudaError_t grow(void **p, size_t &have, size_t need, cudaStream_t st) {
   if (need <= have) return cudaSuccess;
-  if (*p) cudaFree(*p);
+  if (*p) cudaFreeAsync(*p, st);
   *p = nullptr;
   have = 0;
-  cudaError_t e = cudaMalloc(p, need);
+  cudaError_t e = cudaMallocAsync(p, need, st);
   if (e == cudaSuccess) have = need;
   return e;
 }
@@ -920,9 +922,9 @@ struct Runner {
     const int NE = E[k] * (E[k] + 1) / 2;
     TLevel &T = w.lv[k];
     T.cap = cap[k];
-    cudaError_t e = grow((void **)&T.K, w.kbytes[k], (size_t)L * NE * cap[k] * sizeof(double2));
-    if (e == cudaSuccess) e = grow((void **)&T.logc, w.lbytes[k], (size_t)L * cap[k] * sizeof(double2));
-    if (e == cudaSuccess) e = grow((void **)&T.coef, w.cbytes[k], (size_t)cap[k] * sizeof(double));
+    cudaError_t e = grow((void **)&T.K, w.kbytes[k], (size_t)L * NE * cap[k] * sizeof(double2), st);
+    if (e == cudaSuccess) e = grow((void **)&T.logc, w.lbytes[k], (size_t)L * cap[k] * sizeof(double2), st);
+    if (e == cudaSuccess) e = grow((void **)&T.coef, w.cbytes[k], (size_t)cap[k] * sizeof(double), st);
     return e;
   }
 
@@ -1122,7 +1124,10 @@ cudaError_t tree_run(const JobDev &J, TreeGroup &g, TreeWork &w, uint64_t ub, ui
     const int NE = R.E[k] * (R.E[k] + 1) / 2;
     const double nbytes = (double)(NE + 1) * L * 16.0 + 8.0;
     uint64_t c = (uint64_t)std::max(1.0, (double)TreeWork::kLevelBudget / nbytes);
-    if (k == 0) c = std::min<uint64_t>(c, (uint64_t)g.npat);
+    // never more than the forest has at this depth (small jobs keep small buffers)
+    double forest = (double)g.npat;
+    for (int l = 0; l < k; ++l) forest *= (double)R.b[l];
+    if ((double)c > forest) c = (uint64_t)forest;
     if (k >= g.k_u && k > 0) c = std::max<uint64_t>(1, c / R.Pk[k]) * R.Pk[k];
     R.cap[k] = c;
     // scratch of the transition into depth k (k >= 1) / of the leaf kernel (k = H - 1)
@@ -1135,24 +1140,24 @@ cudaError_t tree_run(const JobDev &J, TreeGroup &g, TreeWork &w, uint64_t ub, ui
   }
   cudaError_t e = cudaSuccess;
   for (int k = 0; k < H && e == cudaSuccess; ++k) e = R.level_alloc(k);
-  if (e == cudaSuccess) e = tree::grow(&w.scratch, w.scratch_bytes, scratch * sizeof(double2));
-  if (e == cudaSuccess) e = tree::grow(&w.val, w.val_bytes, (size_t)R.cap[H - 1] * sizeof(double2));
-  if (e == cudaSuccess) e = tree::grow(&w.absv, w.abs_bytes, (size_t)R.cap[H - 1] * sizeof(double));
+  if (e == cudaSuccess) e = tree::grow(&w.scratch, w.scratch_bytes, scratch * sizeof(double2), st);
+  if (e == cudaSuccess) e = tree::grow(&w.val, w.val_bytes, (size_t)R.cap[H - 1] * sizeof(double2), st);
+  if (e == cudaSuccess) e = tree::grow(&w.absv, w.abs_bytes, (size_t)R.cap[H - 1] * sizeof(double), st);
   if (e != cudaSuccess) return e;
   return R.run();
 }
 
 void tree_work_free(TreeWork &w) {
   for (auto &l : w.lv) {
-    if (l.K) cudaFree(l.K);
-    if (l.logc) cudaFree(l.logc);
-    if (l.coef) cudaFree(l.coef);
+    if (l.K) cudaFreeAsync(l.K, 0);
+    if (l.logc) cudaFreeAsync(l.logc, 0);
+    if (l.coef) cudaFreeAsync(l.coef, 0);
   }
   w.lv.clear();
   w.kbytes.clear(); w.lbytes.clear(); w.cbytes.clear();
-  if (w.scratch) cudaFree(w.scratch);
-  if (w.val) cudaFree(w.val);
-  if (w.absv) cudaFree(w.absv);
+  if (w.scratch) cudaFreeAsync(w.scratch, 0);
+  if (w.val) cudaFreeAsync(w.val, 0);
+  if (w.absv) cudaFreeAsync(w.absv, 0);
   w.scratch = w.val = w.absv = nullptr;
   w.scratch_bytes = w.val_bytes = w.abs_bytes = 0;
 }
