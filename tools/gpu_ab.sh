@@ -1,9 +1,12 @@
 #!/bin/bash
-# A/B timing of alternative builds (LHAF_LIB_PATH) on the cfg4 slice and cfg5
+# A/B timing of library variants (build/variants/*.so via LHAF_LIB_PATH) on tree workloads, then
+# the tree GPU tests on the working-tree build.  usage: tools/gpu_ab.sh OUTDIR VARIANT...
 cd $GRAFT_REPO_ROOT
+O=gpurun_out/$1; shift
+mkdir -p $O
 for v in "$@"; do
-  echo "== $v"
-  LHAF_LIB_PATH=$PWD/$v timeout 300 python tools/tree_time.py 4 6 64 2 2>&1 | tail -1
-  LHAF_LIB_PATH=$PWD/$v timeout 300 python tools/tree_time.py 5 6 4 2 2>&1 | tail -1
-  LHAF_LIB_PATH=$PWD/$v timeout 300 python tools/tree_time.py 2 6 1 2 2>&1 | tail -2 | head -1
+  for w in "4 6 64 3" "5 6 64 3" "40 6 1 3" "2 6 1 3"; do
+    LHAF_LIB_PATH=build/variants/$v.so timeout 600 python tools/tree_time.py $w 2>&1 | sed "s/^/$v /" >> $O/ab.txt
+  done
 done
+cat $O/ab.txt
