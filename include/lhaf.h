@@ -63,7 +63,8 @@ typedef enum {
  * phantom pair for odd N (reading C7), and the term counts.  mixed = 1 plans the mixed state
  * by the same greedy matching of the doubled pattern (reps, reps) over the 2k modes (reading
  * C11b: same value, measured far better conditioned in FP64); mixed = 2 selects the natural
- * pairing (i, i+k) x reps_i of P:425-428 (reading C11). */
+ * pairing (i, i+k) x reps_i of P:425-428 (reading C11); mixed = 3 (job API, lhaf_rpt_mixed)
+ * searches the matching with the least cancellation (below) -- planned here like mode 1. */
 typedef struct {
   int32_t N;            /* photons = sum reps */
   int32_t H;            /* distinct pairs incl. phantom */
@@ -105,10 +106,15 @@ lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_s
                            const int32_t *reps, int32_t k, int32_t batch, double *out);
 
 /* Mixed-state loop hafnian (S8(a) a13): lhaf of the 2N x 2N A_n formed from the 2k x 2k
- * matrix A2 by repeating rows/cols i and i+k reps[i] times.  Evaluated with the
- * greedy matching of the doubled pattern (mixed mode 1, reading C11b); the natural pairing
- * (i, i+k) x reps_i of P:425-428 is mixed mode 2 of the job API.  A2: 2k*2k c128,
- * gamma2: 2k c128, reps: k int32. */
+ * matrix A2 by repeating rows/cols i and i+k reps[i] times.  Evaluated with mixed mode
+ * 3: every matching gives the same lhaf but not the same cancellation kappa =
+ * sum|term| / |lhaf|, which sets the FP64 error; 16 greedy matchings of the
+ * doubled pattern (reading C11b; ties broken by seeded relabellings of the modes, the first
+ * the identity = mode 1) are each estimated on 32 work units spread over the sieve and the one
+ * with the smallest sum|term| is evaluated (env LHAF_KAPPA_CANDIDATES / LHAF_KAPPA_SAMPLES).
+ * Mode 1 (the identity candidate alone) and the natural pairing (i, i+k) x reps_i of
+ * P:425-428 (mode 2) are selectable through the job API.  In precise mode the natural pairing
+ * is used.  A2: 2k*2k c128, gamma2: 2k c128, reps: k int32. */
 lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t *reps,
                            int32_t k, double out[2]);
 
@@ -234,8 +240,9 @@ lhaf_status lhaf_rpt_batch_dev(const double *A_dev, const double *gamma_dev, int
 
 /* ---- Jobs: a planned, device-resident evaluation (for timing and multi-rank control) ----
  * lhaf_job_create plans and uploads a batch (mixed = 1: the mixed state over A2 / gamma2 by
- * the greedy matching of the doubled pattern, mixed = 2: by the natural pairing; each reps
- * row of length k).  lhaf_job_run evaluates work units [unit_begin, unit_end) into
+ * the greedy matching of the doubled pattern, mixed = 2: by the natural pairing, mixed = 3:
+ * by the matching search of lhaf_rpt_mixed -- host inputs, gamma_stride 0, FP64 mode; it runs
+ * candidate sample evaluations on the device during the call; each reps row of length k).  lhaf_job_run evaluates work units [unit_begin, unit_end) into
  * the job's chunk-partial array (zeroed by lhaf_job_reset); lhaf_job_finalize sums the
  * partials in chunk order (double-double) and writes batch*2 doubles to out (host pointer if
  * out_is_device == 0).  One work unit = a fixed, rank-independent chunk of one pattern's

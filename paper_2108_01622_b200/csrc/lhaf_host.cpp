@@ -143,8 +143,8 @@ lhaf_status make_plan(const int32_t *reps, int k, int mixed, Plan &P) {
   if (N > 4 * LHAF_MAX_DEGREE) return fail(LHAF_E_TOO_LARGE, "N = %ld photons too large", N);
   P.N = (int)N;
   // precise mode plans mixed states by the natural pairing (lhaf_set_precision, reading C11)
-  if (mixed == 1 && g_ctx.precision == 1) mixed = 2;
-  if (mixed == 1) {
+  if ((mixed == 1 || mixed == 3) && g_ctx.precision == 1) mixed = 2;
+  if (mixed == 1 || mixed == 3) {  // (3: the matching search needs A: job_create_impl)
     // mixed state, default: the greedy matching of the doubled pattern (reps, reps) over the
     // 2k modes (the same lhaf as the natural pairing; far better conditioned in FP64 -- the
     // BASELINE cfg5 sum is rounding noise with the natural pairing)
@@ -330,12 +330,25 @@ static cudaError_t upload(T **dst, const std::vector<T> &v) {
   return e;
 }
 
+static lhaf_status mixed_kappa_plan(const double *A2, const double *g2, const int32_t *reps, int k,
+                                    Plan &best, double *best_est);
 static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t gamma_stride,
                                    const int32_t *reps, int k, int batch, int mixed, bool on_device,
                                    lhaf_job **out, const std::vector<Plan> *plans_in = nullptr) {
   if (!A || !gamma || (!reps && !plans_in) || !out) return fail(LHAF_E_ARG, "null pointer argument");
   if (k < 0 || k > LHAF_MAX_MODES) return fail(LHAF_E_ARG, "k = %d out of range", k);
   if (batch < 0) return fail(LHAF_E_ARG, "batch = %d < 0", batch);
+  if (mixed < 0 || mixed > 3) return fail(LHAF_E_ARG, "mixed = %d (0 pure, 1 greedy doubled, 2 natural, 3 searched)", mixed);
+  if (mixed == 3 && !plans_in && g_ctx.precision == 0 && !on_device && gamma_stride == 0) {
+    // kappa-aware matching per pattern (mixed_kappa_plan), then the job on those plans
+    std::vector<Plan> plans(batch);
+    for (int b = 0; b < batch; ++b) {
+      lhaf_status s0 = check_symmetric(A, 2 * k);
+      if (s0 == LHAF_OK) s0 = mixed_kappa_plan(A, gamma, reps + (size_t)b * k, k, plans[b], nullptr);
+      if (s0 != LHAF_OK) return s0;
+    }
+    return job_create_impl(A, gamma, 0, nullptr, k, batch, 1, false, out, &plans);
+  }
   const int kdim = mixed ? 2 * k : k;
   if (gamma_stride != 0 && gamma_stride < kdim)
     return fail(LHAF_E_ARG, "gamma_stride %lld < row length %d", (long long)gamma_stride, kdim);
@@ -587,11 +600,8 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
   j->variant = use_tree ? 6 : g_ctx.variant ? g_ctx.variant : choose_variant(j->e_max, j->n_max);
   j->prec = g_ctx.precision;
   if (j->prec && !use_tree) j->variant = 5;  // the precise tail lives in the v5 kernel (every E <= 64)
-  // inclusion/exclusion: excluded pairs are zero columns -- v5 deletes them per term (reduction
-  // at the term's own size), which is where ET's cost advantage comes from
-  bool any_et = false;
-  for (const auto &D : j->descs) any_et = any_et || (D.flags & FLAG_ET);
-  if (any_et && g_ctx.variant == 0 && v5_supported(j->e_max)) j->variant = 5;
+  // inclusion/exclusion: excluded pairs are deleted -- on the tree (default: a deleted
+  // pair's children copy the parent's leading block) or per term on v5 (lhaf_set_kernel(5))
   if (j->variant == 0 || (j->variant == 5 && !v5_supported(j->e_max))) j->variant = 3;
   if (j->prec && j->variant != 5 && j->variant != 6) {
     job_free(j);
@@ -664,6 +674,77 @@ static lhaf_status evaluate(lhaf_job *j, double *out_host, double *out_dev, cuda
   if (out_host)
     CUDA_TRY(cudaMemcpyAsync(out_host, dst, (size_t)j->batch * sizeof(double2), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return LHAF_OK;
+}
+
+// ------------------------------------------------------------------ kappa-aware matching
+// Every matching of the repeated rows gives the same loop hafnian, but not the same
+// cancellation: kappa = sum|term| / |lhaf| sets the FP64 error of the sum, and for
+// the BASELINE mixed state it varies ~40x between matchings that differ only in how the greedy
+// rule breaks ties.  Mixed mode 3: C candidate matchings -- the greedy matching
+// of the doubled pattern with the 2k modes relabelled by seeded permutations (candidate 0 =
+// the identity, i.e. mode 1) -- each estimated by evaluating S work units spread over its sieve
+// (sum|term| of the sample x units / S), and the one with the smallest estimate is kept.
+static uint64_t splitmix64(uint64_t &x) {
+  uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+static lhaf_status mixed_kappa_plan(const double *A2, const double *g2, const int32_t *reps, int k,
+                                    Plan &best, double *best_est) {
+  const int C = std::max(1, env_int("LHAF_KAPPA_CANDIDATES", 16));
+  const int S = std::max(1, env_int("LHAF_KAPPA_SAMPLES", 32));
+  const int k2 = 2 * k;
+  std::vector<int32_t> r2(k2);
+  for (int i = 0; i < k; ++i) r2[i] = r2[i + k] = reps[i];
+  double best_abs = INFINITY;
+  bool have = false;
+  for (int c = 0; c < C; ++c) {
+    std::vector<int> lab(k2);  // mode i gets label lab[i]
+    for (int i = 0; i < k2; ++i) lab[i] = i;
+    uint64_t seed = 0x5EEDull + (uint64_t)c;
+    for (int i = k2 - 1; c > 0 && i > 0; --i) std::swap(lab[i], lab[splitmix64(seed) % (uint64_t)(i + 1)]);
+    std::vector<int32_t> rl(k2);
+    std::vector<int> inv(k2);
+    for (int i = 0; i < k2; ++i) { rl[lab[i]] = r2[i]; inv[lab[i]] = i; }
+    Plan P;
+    lhaf_status s = make_plan(rl.data(), k2, 0, P);
+    if (s != LHAF_OK) return s;
+    for (int h = 0; h < P.H; ++h) {
+      P.p[h] = P.p[h] >= 0 ? inv[P.p[h]] : -1;
+      P.q[h] = P.q[h] >= 0 ? inv[P.q[h]] : -1;
+    }
+    if (P.leftover >= 0) P.leftover = inv[P.leftover];
+    std::vector<Plan> plans{P};
+    lhaf_job *j = nullptr;
+    s = job_create_impl(A2, g2, 0, nullptr, k, 1, 1, false, &j, &plans);
+    if (s != LHAF_OK) return s;
+    double est = 0.0;
+    if (j->units > 0) {
+      const uint64_t U = j->units, n = std::min<uint64_t>(U, (uint64_t)S);
+      cudaError_t e = cudaMemsetAsync(j->d_partials, 0, U * sizeof(Partial), 0);
+      for (uint64_t t = 0; t < n && e == cudaSuccess; ++t) {
+        const uint64_t u = (uint64_t)(((double)t + 0.5) * (double)U / (double)n);
+        e = run_sieve(j, u, u + 1, 0);
+      }
+      if (e == cudaSuccess) e = launch_finalize(j->dev(), j->d_out, j->d_abs, 0);
+      double a = 0.0;
+      if (e == cudaSuccess) e = cudaMemcpy(&a, j->d_abs, sizeof(double), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) {
+        job_free(j);
+        return fail(LHAF_E_CUDA, "matching search: %s", cudaGetErrorString(e));
+      }
+      est = a * (double)U / (double)n;
+    }
+    job_free(j);
+    if (!have || est < best_abs) { best_abs = est; best = P; have = true; }
+  }
+  if (best_est) *best_est = best_abs;
   return LHAF_OK;
 }
 
@@ -1115,7 +1196,7 @@ lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   if (!out) return fail(LHAF_E_ARG, "null output");
   lhaf_job *j = nullptr;
-  lhaf_status s = job_create_impl(A2, gamma2, 0, reps, k, 1, 1, false, &j);
+  lhaf_status s = job_create_impl(A2, gamma2, 0, reps, k, 1, 3, false, &j);
   if (s != LHAF_OK) return s;
   double tmp[2];
   s = evaluate(j, tmp, nullptr, 0);

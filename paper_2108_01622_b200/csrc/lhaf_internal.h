@@ -113,7 +113,7 @@ cudaError_t launch_terms_v5(const JobDev &job, int e_max, int ntl_max, int n_max
 // Variant 6 (lhaf_tree.cu): the sieve terms of a pattern as the leaves of a tree that shares
 // every prefix of eliminated pairs (symmetric 2x2-block Schur complements of power series).
 namespace tree {
-struct TLevel {   // the nodes of one depth: K[(s * NE + e) * cap + node], logc[s * cap + node]
+struct TLevel {   // the nodes of one depth: K[(node * NE + e) * L + s], logc[node * L + s]
   double2 *K;
   double2 *logc;
   double *coef;   // sign * prod C(eta, k) of the node's path
@@ -133,6 +133,9 @@ struct TreeWork {             // device buffers of the tree driver, kept across 
   static constexpr size_t kLevelBudget = (size_t)512 << 20;  // bytes per depth
   std::vector<tree::TLevel> lv;
   std::vector<size_t> kbytes, lbytes, cbytes;
+  // per depth: node-level series of the next pivot (Delta; at the last depth Delta, P, N0)
+  std::vector<void *> aux;
+  std::vector<size_t> abytes;
   void *scratch = nullptr, *val = nullptr, *absv = nullptr;
   size_t scratch_bytes = 0, val_bytes = 0, abs_bytes = 0;
 };

@@ -67,31 +67,79 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // acc[k] += sum_{s + q = t0 + k - sh} a[s] b[q]   (0 <= s < La, 0 <= q < Lb; k < TB)
 // The b operand streams through a TB-slot window in registers (one new value per step, slot
 // indices resolved at compile time by unrolling the steps by TB): two loads per TB complex MACs.
+// acc[k] += av * w[(k - rho) mod TB] for the TB outputs, the first FMA of every output issued
+// before the second (the two FMAs of one complex component are dependent: this order keeps
+// 2 TB independent chains between them)
+#ifndef LHAF_TWOPASS
+#define LHAF_TWOPASS 1
+#endif
+__device__ __forceinline__ void cfma_row(double2 (&acc)[TB], double2 av, const double2 (&w)[TB], const int RHO) {
+  if (!LHAF_TWOPASS) {
+#pragma unroll
+    for (int k = 0; k < TB; ++k) acc[k] = cfma(av, w[(k - RHO + TB) % TB], acc[k]);
+    return;
+  }
+  double2 t[TB];
+#pragma unroll
+  for (int k = 0; k < TB; ++k) {
+    const double2 b = w[(k - RHO + TB) % TB];
+    t[k].x = fma(av.x, b.x, acc[k].x);
+    t[k].y = fma(av.x, b.y, acc[k].y);
+  }
+#pragma unroll
+  for (int k = 0; k < TB; ++k) {
+    const double2 b = w[(k - RHO + TB) % TB];
+    acc[k].x = fma(-av.y, b.y, t[k].x);
+    acc[k].y = fma(av.y, b.x, t[k].y);
+  }
+}
+
+// Steps s <= base feed every output of the block (the windowed loop); the last steps s = base + j
+// (j = 1 .. TB-1) feed only outputs k >= j with q = k - j (the triangle of the block, unrolled on
+// b[0 .. TB-2] in registers, so that no MAC is spent on a zero).
 __device__ __forceinline__ void conv_acc(double2 (&acc)[TB], int t0, int sh, SR a, int La, SR b, int Lb) {
   const int base = t0 - sh;
   const int s_lo = max(0, base - (Lb - 1));
   const int s_hi = min(La - 1, base + TB - 1);
   if (s_lo > s_hi) return;
-  const int Q0 = base - s_lo;  // q of output k = 0 at step 0
-  double2 w[TB];
+  const int s_top = min(s_hi, base);
+  if (s_lo <= s_top) {
+    // window: output k reads b[Q0 + k - r] at step r; for s <= base every index the steps load
+    // lies in [0, Lb) (q = base - s >= 0 and q <= Q0 <= Lb - 1): only the first fill checks
+    const int Q0 = base - s_lo;  // q of output k = 0 at step 0
+    double2 w[TB];
 #pragma unroll
-  for (int k = 0; k < TB; ++k) {
-    const int q = Q0 + k;
-    w[k] = (q >= 0 && q < Lb) ? at(b, q) : c0();
-  }
-  const int nsteps = s_hi - s_lo + 1;
-  for (int r0 = 0; r0 < nsteps; r0 += TB) {
+    for (int k = 0; k < TB; ++k) {
+      const int q = Q0 + k;
+      w[k] = (q < Lb) ? at(b, q) : c0();
+    }
+    const int nsteps = s_top - s_lo + 1;
+    const double2 *ap = a.p + (int64_t)s_lo * a.st, *bp = b.p + (int64_t)Q0 * b.st;
+    for (int r0 = 0; r0 < nsteps; r0 += TB) {
 #pragma unroll
-    for (int rho = 0; rho < TB; ++rho) {
-      const int r = r0 + rho;
-      if (r < nsteps) {
-        if (r > 0) {  // the value output 0 needs now; output k reads slot (k - r) mod TB
-          const int q = Q0 - r;
-          w[(TB - rho) % TB] = (q >= 0 && q < Lb) ? at(b, q) : c0();
+      for (int rho = 0; rho < TB; ++rho) {
+        const int r = r0 + rho;
+        if (r < nsteps) {
+          if (r > 0) w[(TB - rho) % TB] = bp[-(int64_t)r * b.st];
+          cfma_row(acc, ap[(int64_t)r * a.st], w, rho);
         }
-        const double2 av = at(a, s_lo + r);
+      }
+    }
+  }
+  {  // triangle
+    const int jlo = max(1, -base), jhi = s_hi - base;
+    if (jlo <= jhi) {
+      double2 bq[TB - 1];
 #pragma unroll
-        for (int k = 0; k < TB; ++k) acc[k] = cfma(av, w[(k - rho + TB) % TB], acc[k]);
+      for (int q = 0; q < TB - 1; ++q) bq[q] = (q < Lb && q <= TB - 1 - jlo) ? at(b, q) : c0();
+      const double2 *ap = a.p + (int64_t)base * a.st;
+#pragma unroll
+      for (int j = 1; j < TB; ++j) {
+        if (j >= jlo && j <= jhi) {
+          const double2 av = ap[(int64_t)j * a.st];
+#pragma unroll
+          for (int k = j; k < TB; ++k) acc[k] = cfma(av, bq[k - j], acc[k]);
+        }
       }
     }
   }
@@ -384,6 +432,7 @@ struct TStep {  // parent depth k -> children at depth k + 1, one chunk of child
   double2 *S;      // fallback scratch
   double2 *T;      // fallback T: [nc][2][E-2][L]
   int G;           // children per block of tree_bc_k
+  double2 *auxp;   // parents' Delta = K_ab^2 - K_aa K_bb at auxp[parent slot * L] (tree_delta_r)
 };
 
 __device__ __forceinline__ void child_of(const TStep &P, uint64_t i, uint64_t &ps, int &kh, int &w) {
@@ -393,13 +442,14 @@ __device__ __forceinline__ void child_of(const TStep &P, uint64_t i, uint64_t &p
   w = P.eta - P.wmul * kh;
 }
 
-// Delta = K_ab^2 - K_aa K_bb of every parent of the chunk (shared by its children: the weight
-// enters only D = 1 - 2 w lam K_ab + w^2 lam^2 Delta), into P.S[(parent - first parent) * L]
+// Delta = K_ab^2 - K_aa K_bb of parent slots [p0, p0 + np) (shared by its children: the weight
+// enters only D = 1 - 2 w lam K_ab + w^2 lam^2 Delta), into P.auxp[slot * L].  Used where no
+// tree_bc_k produced it (the root depth, the fallback update kernels).
 template <int LM>
-__global__ void __launch_bounds__(128) tree_delta_r(TStep P, uint64_t np) {
+__global__ void __launch_bounds__(128) tree_delta_r(TStep P, uint64_t p0, uint64_t np) {
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
   if (i >= np) return;
-  const uint64_t ps = P.c0 / P.b + i - P.pbase;
+  const uint64_t ps = p0 + i;
   const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
   const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
   double2 A[LM], B[LM];
@@ -408,7 +458,7 @@ __global__ void __launch_bounds__(128) tree_delta_r(TStep P, uint64_t np) {
   rr_acc(A, B, B, L);
   rload(B, Kp + (int64_t)tri(a, a) * L, L);
   rs_op(A, Kp + (int64_t)tri(b, b) * L, B, L, -1.0);
-  rstore(P.S + (int64_t)i * L, A, L);
+  rstore(P.auxp + (int64_t)ps * L, A, L);
 }
 
 // Per child: D_w, R = 1/D_w, t log D_w (child log c), Q.  Series in two register arrays; each
@@ -424,7 +474,7 @@ __global__ void __launch_bounds__(128) tree_pivot_r(TStep P) {
   const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
   const double2 *Kaa = Kp + (int64_t)tri(a, a) * L, *Kbb = Kp + (int64_t)tri(b, b) * L,
                 *Kab = Kp + (int64_t)tri(b, a) * L;
-  const double2 *Dl = P.S + (int64_t)((P.c0 + i) / P.b - P.c0 / P.b) * L;
+  const double2 *Dl = P.auxp + (int64_t)ps * L;
   const double2 *lp = P.par.logc + (int64_t)ps * L;
   double2 *lc = P.ch.logc + (int64_t)i * L;
   double2 *Q = P.Q + (int64_t)i * 3 * L;
@@ -462,6 +512,81 @@ __global__ void __launch_bounds__(128) tree_pivot_r(TStep P) {
   }
 }
 
+// The same pivot with the operands staged in shared memory: the parents' K_ab, Delta, K_aa (then
+// K_bb in Delta's place) are copied by the whole block with coalesced 16-byte copies, so the
+// register-array products read shared memory instead of issuing one L2 load per coefficient.
+// Children of a block span at most (PV_THREADS - 1) / b + 2 parents (b >= 2, host-checked); a
+// parent's series sits at an odd stride (in 16-byte units) so that the lanes of a quarter-warp
+// hit distinct banks.  t log D is the in-place product sum_s s D_s R_{t-s} (no recursion).
+constexpr int PV_THREADS = 128;
+__host__ __device__ __forceinline__ int pv_stride(int L) { return L | 1; }
+__host__ __device__ __forceinline__ int pv_parents(int b) { return (PV_THREADS - 1) / b + 2; }
+template <int LM>
+__global__ void __launch_bounds__(PV_THREADS, 2) tree_pivot_s(TStep P) {
+  extern __shared__ double2 sv[];
+  const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
+  const int SP = pv_stride(L), NPM = pv_parents(P.b);
+  double2 *bKab = sv, *bX = sv + (int64_t)NPM * SP, *bKaa = sv + 2 * (int64_t)NPM * SP;
+  const uint64_t i0 = (uint64_t)blockIdx.x * PV_THREADS, i = i0 + threadIdx.x;
+  const bool active = i < P.nc;
+  uint64_t psf, psl; int kh, w;
+  child_of(P, min(i0 + PV_THREADS - 1, P.nc - 1), psl, kh, w);
+  child_of(P, i0, psf, kh, w);
+  const int NP = (int)(psl - psf) + 1;
+  for (int c = threadIdx.x; c < NP * L; c += PV_THREADS) {
+    const int p = c / L, s = c - p * L;
+    const double2 *Kp = P.par.K + (int64_t)(psf + p) * NE * L;
+    cp_async16(bKab + p * SP + s, Kp + (int64_t)tri(b, a) * L + s);
+    cp_async16(bKaa + p * SP + s, Kp + (int64_t)tri(a, a) * L + s);
+    cp_async16(bX + p * SP + s, P.auxp + (int64_t)(psf + p) * L + s);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  uint64_t ps = 0;
+  if (active) child_of(P, i, ps, kh, w);
+  const int pl = (int)(ps - psf);
+  const double wd = (double)w, w2 = wd * wd;
+  double2 A[LM], B[LM];
+  if (active && w != 0) {
+    rdet(A, bKab + pl * SP, bX + pl * SP, w, L);                // A = D_w
+    rrec(B, A, L, 1.0, 0.0, -1.0, false);                     // B = 1/D
+    rtlog_inplace(A, B, L);                                   // A = t log D_t
+    const double2 *lp = P.par.logc + (int64_t)ps * L;
+    double2 *lc = P.ch.logc + (int64_t)i * L;
+#pragma unroll
+    for (int t = 0; t < LM; ++t)
+      if (t < L) lc[t] = t ? cadd(lp[t], cscale(A[t], 1.0 / t)) : lp[t];
+  } else if (active) {  // deleted pair: D = 1, Q = 0
+    const double2 *lp = P.par.logc + (int64_t)ps * L;
+    double2 *lc = P.ch.logc + (int64_t)i * L, *Q = P.Q + (int64_t)i * 3 * L;
+    for (int t = 0; t < L; ++t) { lc[t] = lp[t]; Q[t] = Q[L + t] = Q[2 * L + t] = c0(); }
+  }
+  if (active) P.ch.coef[i] = P.par.coef[ps] * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
+  __syncthreads();  // Delta consumed: K_bb takes its buffer
+  for (int c = threadIdx.x; c < NP * L; c += PV_THREADS) {
+    const int p = c / L, s = c - p * L;
+    cp_async16(bX + p * SP + s, P.par.K + ((int64_t)(psf + p) * NE + tri(b, b)) * L + s);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (!active || w == 0) return;
+  double2 *Q = P.Q + (int64_t)i * 3 * L;
+#pragma unroll 1
+  for (int qi = 0; qi < 3; ++qi) {                            // lam K R for K = Kbb, Kaa, Kab
+    rz(A);
+    rs_op(A, (qi == 0 ? bX : qi == 1 ? bKaa : bKab) + pl * SP, B, L, 1.0);
+#pragma unroll
+    for (int t = 0; t < LM; ++t) {
+      if (t < L) {
+        const double2 m = t ? A[t - 1] : c0();
+        if (qi == 0) Q[t] = cscale(m, w2);                                           // q11
+        else if (qi == 1) Q[2 * L + t] = cscale(m, w2);                              // q22
+        else Q[L + t] = make_double2(wd * B[t].x - w2 * m.x, wd * B[t].y - w2 * m.y);  // q12
+      }
+    }
+  }
+}
+
 // generic pivot (any L): the blocked series routines above with per-child scratch in HBM
 __global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
@@ -477,9 +602,10 @@ __global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
 }
 
 // T_j = Q (u_j, x_j)^T and K'_ij = K_ij + lam (u_i T1_j + x_i T2_j) for a group of G children:
-// the parent rows (u, x) and the children's Q in shared memory, T written there, then the
-// packed lower triangle of every child.  Shared layout per child: U[Ep][L] X[Ep][L] Q[3][L]
-// T1[Ep][L] T2[Ep][L].
+// the parent rows (u, x) -- once per parent, shared by its children in the group -- and the
+// children's Q in shared memory, T written there, then the packed lower triangle of every child.
+// Shared layout: parents U[Ep][L] X[Ep][L] (bc_smem_parents of them), then per child Q[3][L]
+// T1[Ep][L] T2[Ep][L].  The block size (blockDim.x <= BC_THREADS) and G come from bc_choose.
 #ifndef LHAF_BC_THREADS
 #define LHAF_BC_THREADS 128
 #endif
@@ -490,27 +616,35 @@ __global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
 #define LHAF_BC_SMEM_KB 72
 #endif
 constexpr int BC_THREADS = LHAF_BC_THREADS;
+// parents a group of G consecutive children can span (b children per parent)
+__host__ __device__ __forceinline__ int bc_smem_parents(int G, int b) { return min(G, (G - 1) / b + 2); }
 __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   extern __shared__ double2 sm[];
   const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1, Ep = E - 2;
   const int NEc = Ep * (Ep + 1) / 2;
-  const int per = (4 * Ep + 3) * L;
+  const int per = (2 * Ep + 3) * L;
   const uint64_t g0 = (uint64_t)blockIdx.x * P.G;
   const int G = (int)min((uint64_t)P.G, P.nc - g0);
-  const int tid = threadIdx.x;
-  // stage
-  for (int g = 0; g < G; ++g) {
-    uint64_t ps; int kh, w;
-    child_of(P, g0 + g, ps, kh, w);
-    const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  uint64_t ps0; int kh0, w0;
+  child_of(P, g0, ps0, kh0, w0);
+  uint64_t psl; int khl, wl;
+  child_of(P, g0 + G - 1, psl, khl, wl);
+  const int NP = (int)(psl - ps0) + 1;
+  double2 *cbase = sm + (int64_t)bc_smem_parents(P.G, P.b) * 2 * Ep * L;
+  // stage: parent rows, then the children's Q
+  for (int p = 0; p < NP; ++p) {
+    const double2 *Kp = P.par.K + (int64_t)(ps0 + p) * NE * L;
     const double2 *ur = Kp + (int64_t)tri(a, 0) * L, *xr = Kp + (int64_t)tri(b, 0) * L;
-    const double2 *qr = P.Q + (int64_t)(g0 + g) * 3 * L;
-    double2 *base = sm + (int64_t)g * per;
-    for (int t = tid; t < Ep * L; t += BC_THREADS) {
-      cp_async16(base + t, ur + t);
-      cp_async16(base + Ep * L + t, xr + t);
+    double2 *pb = sm + (int64_t)p * 2 * Ep * L;
+    for (int t = tid; t < Ep * L; t += nth) {
+      cp_async16(pb + t, ur + t);
+      cp_async16(pb + Ep * L + t, xr + t);
     }
-    for (int t = tid; t < 3 * L; t += BC_THREADS) cp_async16(base + 2 * Ep * L + t, qr + t);
+  }
+  for (int g = 0; g < G; ++g) {
+    const double2 *qr = P.Q + (int64_t)(g0 + g) * 3 * L;
+    for (int t = tid; t < 3 * L; t += nth) cp_async16(cbase + (int64_t)g * per + t, qr + t);
   }
   cp_async_wait_all();
   __syncthreads();
@@ -518,17 +652,16 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   // tasks are split by output blocks, paired (p, nb - 1 - p) so that every task does about the
   // same work (the products are triangular): PB parts per series
   const int nbB = (Lo + TB - 1) / TB, PB = (nbB + 1) / 2;
-  for (int task = tid; task < G * 2 * Ep * PB; task += BC_THREADS) {
+  for (int task = tid; task < G * 2 * Ep * PB; task += nth) {
     const int part = task % PB, tk = task / PB;
     const int g = tk / (2 * Ep), r = tk - g * 2 * Ep, j = r >> 1, which = r & 1;
-    {
-      uint64_t ps; int kh, w;
-      child_of(P, g0 + g, ps, kh, w);
-      if (w == 0) continue;  // deleted pair: the child is the parent's leading block
-    }
-    double2 *base = sm + (int64_t)g * per;
-    const double2 *U = base, *X = base + Ep * L, *Qs = base + 2 * Ep * L;
-    double2 *T = base + (2 * Ep + 3) * L + (int64_t)which * Ep * L + (int64_t)j * L;
+    uint64_t ps; int kh, w;
+    child_of(P, g0 + g, ps, kh, w);
+    if (w == 0) continue;  // deleted pair: the child is the parent's leading block
+    const double2 *U = sm + (int64_t)(ps - ps0) * 2 * Ep * L, *X = U + Ep * L;
+    double2 *base = cbase + (int64_t)g * per;
+    const double2 *Qs = base;
+    double2 *T = base + 3 * L + (int64_t)which * Ep * L + (int64_t)j * L;
     // T1 = q11 u + q12 x ; T2 = q12 u + q22 x
     const SR qa{Qs + (which ? L : 0), 1}, qb{Qs + (which ? 2 * L : L), 1};
     for (int bi = 0; bi < 2; ++bi) {
@@ -547,7 +680,7 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   }
   __syncthreads();
   const int nbC = (L + TB - 1) / TB, PC = (nbC + 1) / 2;
-  for (int task = tid; task < G * NEc * PC; task += BC_THREADS) {
+  for (int task = tid; task < G * NEc * PC; task += nth) {
     const int part = task % PC, tk = task / PC;
     const int g = tk / NEc, e = tk - g * NEc;
     int ii = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
@@ -556,8 +689,8 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
     const int jj = e - tri(ii, 0);
     uint64_t ps; int kh, w;
     child_of(P, g0 + g, ps, kh, w);
-    const double2 *base = sm + (int64_t)g * per;
-    const double2 *U = base, *X = base + Ep * L, *T1 = base + (2 * Ep + 3) * L, *T2 = T1 + Ep * L;
+    const double2 *U = sm + (int64_t)(ps - ps0) * 2 * Ep * L, *X = U + Ep * L;
+    const double2 *T1 = cbase + (int64_t)g * per + 3 * L, *T2 = T1 + Ep * L;
     const double2 *K = P.par.K + ((int64_t)ps * NE + e) * L;
     double2 *out = P.ch.K + ((int64_t)(g0 + g) * NEc + e) * L;
     for (int bi = 0; bi < 2; ++bi) {
@@ -902,6 +1035,60 @@ static int reg_limit() {  // LHAF_TREE_REGL: largest L for the register-array ke
   return v;
 }
 
+static size_t bc_smem(int Ep, int b, int L, int G) {
+  return ((size_t)bc_smem_parents(G, b) * 2 * Ep + (size_t)G * (2 * Ep + 3)) * L * sizeof(double2);
+}
+// Children per block G and threads per block for tree_bc_k: the choice that maximises a
+// throughput model -- children per block x resident blocks per SM / task rounds per block
+// (each phase's tasks are spread over the block's threads; a round = one task per thread),
+// discounted below 12 resident warps per SM.  LHAF_BC_MODEL=0: the fixed heuristic (128
+// threads, about two tasks each) -- an A/B knob.
+static size_t bc_choose(int Ep, int NEc, int b, int L, int &Gbest, int &nbest) {
+  static int regs = 0;
+  if (!regs) {
+    cudaFuncAttributes fa;
+    regs = (cudaFuncGetAttributes(&fa, tree_bc_k) == cudaSuccess && fa.numRegs > 0) ? fa.numRegs : 168;
+    regs = (regs + 7) / 8 * 8;
+  }
+  const int Lo = L - 1, PB = ((Lo + TB - 1) / TB + 1) / 2, PC = ((L + TB - 1) / TB + 1) / 2;
+  const size_t cap = (size_t)LHAF_BC_SMEM_KB << 10;
+  static const int model = [] {
+    const char *e = getenv("LHAF_BC_MODEL");
+    return e ? atoi(e) : 1;
+  }();
+  if (!model) {
+    int G = std::max(1, 2 * 128 / (2 * Ep + NEc) + 1);
+    while (G > 1 && bc_smem(Ep, b, L, G) > cap) --G;
+    Gbest = G; nbest = 128;
+    return bc_smem(Ep, b, L, G);
+  }
+  double best = -1.0;
+  size_t bestb = bc_smem(Ep, b, L, 1);
+  Gbest = 1; nbest = 128;
+  for (int nth = 64; nth <= BC_THREADS; nth += 32)
+    for (int G = 1; G <= 64; ++G) {
+      const size_t sb = bc_smem(Ep, b, L, G);
+      if (sb > (size_t)(220 << 10)) break;
+      if (G > 1 && sb > cap) break;
+      auto rounds = [&](long t) { return (double)((t + nth - 1) / nth); };
+      const double r = rounds((long)G * 2 * Ep * PB) + rounds((long)G * NEc * PC);
+      const int bl_smem = (int)((228u << 10) / (sb + 1024)), bl_reg = 65536 / (regs * nth);
+      const int blocks = std::max(1, std::min(std::min(bl_smem, bl_reg), std::min(32, 64 / (nth / 32))));
+      const double warps = (double)blocks * nth / 32.0;
+      const double score = (double)blocks * G / r * std::min(1.0, warps / 12.0);
+      if (score > best) { best = score; Gbest = G; nbest = nth; bestb = sb; }
+    }
+  return bestb;
+}
+
+static bool pivot_staged() {  // LHAF_TREE_PIVOT=0: the register kernel reading HBM (A/B knob)
+  static const bool v = [] {
+    const char *e = getenv("LHAF_TREE_PIVOT");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 struct Runner {
   const JobDev &J;
   TreeGroup &g;
@@ -925,6 +1112,7 @@ struct Runner {
     cudaError_t e = grow((void **)&T.K, w.kbytes[k], (size_t)L * NE * cap[k] * sizeof(double2), st);
     if (e == cudaSuccess) e = grow((void **)&T.logc, w.lbytes[k], (size_t)L * cap[k] * sizeof(double2), st);
     if (e == cudaSuccess) e = grow((void **)&T.coef, w.cbytes[k], (size_t)cap[k] * sizeof(double), st);
+    if (e == cudaSuccess) e = grow(&w.aux[k], w.abytes[k], (size_t)L * cap[k] * sizeof(double2), st);
     return e;
   }
 
@@ -961,6 +1149,18 @@ struct Runner {
       lo = std::max(lo, U0 / q);
       hi = std::min(hi, (U1 - 1) / q + 1);
     }
+    const int rl = reg_limit();
+    const bool regk = L <= 40 && L <= rl;
+    if (regk) {  // Delta of the parents of this expansion (shared by their children's pivots)
+      const uint64_t p0 = lo / nb - gs, np = (hi - 1) / nb - gs - p0 + 1;
+      TStep D;
+      D.par = w.lv[k]; D.L = L; D.E = E[k]; D.auxp = (double2 *)w.aux[k];
+      ++lhaf::g_launches;
+      if (L <= 16) tree_delta_r<16><<<blocks_for(np), 128, 0, st>>>(D, p0, np);
+      else if (L <= 24) tree_delta_r<24><<<blocks_for(np), 128, 0, st>>>(D, p0, np);
+      else if (L <= 32) tree_delta_r<32><<<blocks_for(np), 128, 0, st>>>(D, p0, np);
+      else tree_delta_r<40><<<blocks_for(np), 128, 0, st>>>(D, p0, np);
+    }
     uint64_t chunk = cap[k + 1];
     for (uint64_t c = lo; c < hi; c += chunk) {
       const uint64_t n = std::min(chunk, hi - c);
@@ -971,36 +1171,40 @@ struct Runner {
       P.c0 = c;
       P.nc = n;
       P.L = L; P.E = E[k]; P.b = b[k]; P.dmin = dmin[k]; P.eta = eta[k]; P.wmul = g.wmul;
+      P.auxp = (double2 *)w.aux[k];
       const int Ep = E[k] - 2, NEc = Ep * (Ep + 1) / 2;
       P.Q = (double2 *)w.scratch;
       P.S = P.Q + (size_t)3 * L * n;
       P.T = P.S + (size_t)3 * L * n;
       ++lhaf::g_launches;
-      const int rl = reg_limit();
-      const uint64_t npar = (c + n - 1) / nb - c / nb + 1;
-      if (L <= 40 && L <= rl) ++lhaf::g_launches;
-      if (L <= 16 && L <= rl) {
-        tree_delta_r<16><<<blocks_for(npar), 128, 0, st>>>(P, npar);
-        tree_pivot_r<16><<<blocks_for(n), 128, 0, st>>>(P);
-      } else if (L <= 24 && L <= rl) {
-        tree_delta_r<24><<<blocks_for(npar), 128, 0, st>>>(P, npar);
-        tree_pivot_r<24><<<blocks_for(n), 128, 0, st>>>(P);
-      } else if (L <= 32 && L <= rl) {
-        tree_delta_r<32><<<blocks_for(npar), 128, 0, st>>>(P, npar);
-        tree_pivot_r<32><<<blocks_for(n), 128, 0, st>>>(P);
-      } else if (L <= 40 && L <= rl) {
-        tree_delta_r<40><<<blocks_for(npar), 128, 0, st>>>(P, npar);
-        tree_pivot_r<40><<<blocks_for(n), 128, 0, st>>>(P);
-      } else {
-        tree_pivot_g<<<blocks_for(n), 128, 0, st>>>(P);
-      }
+      const bool staged = pivot_staged() && nb >= 2;
+      const size_t pv_smem = (size_t)3 * pv_parents((int)nb) * pv_stride(L) * sizeof(double2);
+#define LHAF_PIVOT(LMV)                                                                         \
+  do {                                                                                          \
+    if (staged) {                                                                               \
+      static bool set = false;                                                                  \
+      if (!set) {                                                                               \
+        cudaFuncSetAttribute(tree_pivot_s<LMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10); \
+        set = true;                                                                             \
+      }                                                                                         \
+      tree_pivot_s<LMV><<<(unsigned)((n + PV_THREADS - 1) / PV_THREADS), PV_THREADS, pv_smem, st>>>(P); \
+    } else {                                                                                    \
+      tree_pivot_r<LMV><<<blocks_for(n), 128, 0, st>>>(P);                                      \
+    }                                                                                           \
+  } while (0)
+      if (L <= 16 && regk) LHAF_PIVOT(16);
+      else if (L <= 24 && regk) LHAF_PIVOT(24);
+      else if (L <= 32 && regk) LHAF_PIVOT(32);
+      else if (regk) LHAF_PIVOT(40);
+      else tree_pivot_g<<<blocks_for(n), 128, 0, st>>>(P);
+#undef LHAF_PIVOT
       if (Ep > 0) {
-        const size_t per = (size_t)(4 * Ep + 3) * L * sizeof(double2);
-        int G = std::max(1, std::min(2 * BC_THREADS / (2 * Ep + NEc) + 1, (int)((LHAF_BC_SMEM_KB << 10) / per)));
-        if ((size_t)G * per <= (size_t)(220 << 10)) {
+        int G = 1, nth = 128;  // children and threads per block (bc_choose)
+        const size_t sbytes = bc_choose(Ep, NEc, (int)nb, L, G, nth);
+        if (sbytes <= (size_t)(220 << 10)) {
           P.G = G;
           ++lhaf::g_launches;
-          tree_bc_k<<<(unsigned)((n + G - 1) / G), BC_THREADS, (size_t)G * per, st>>>(P);
+          tree_bc_k<<<(unsigned)((n + G - 1) / G), nth, sbytes, st>>>(P);
         } else {
           lhaf::g_launches += 2;
           tree_tmat_g<<<blocks_for(n * Ep), 128, 0, st>>>(P);
@@ -1138,6 +1342,7 @@ cudaError_t tree_run(const JobDev &J, TreeGroup &g, TreeWork &w, uint64_t ub, ui
     w.lv.resize(H, tree::TLevel{nullptr, nullptr, nullptr, 0});
     w.kbytes.resize(H, 0); w.lbytes.resize(H, 0); w.cbytes.resize(H, 0);
   }
+  if (w.aux.size() < (size_t)H) { w.aux.resize(H, nullptr); w.abytes.resize(H, 0); }
   cudaError_t e = cudaSuccess;
   for (int k = 0; k < H && e == cudaSuccess; ++k) e = R.level_alloc(k);
   if (e == cudaSuccess) e = tree::grow(&w.scratch, w.scratch_bytes, scratch * sizeof(double2), st);
@@ -1155,6 +1360,9 @@ void tree_work_free(TreeWork &w) {
   }
   w.lv.clear();
   w.kbytes.clear(); w.lbytes.clear(); w.cbytes.clear();
+  for (auto &a : w.aux)
+    if (a) cudaFreeAsync(a, 0);
+  w.aux.clear(); w.abytes.clear();
   if (w.scratch) cudaFreeAsync(w.scratch, 0);
   if (w.val) cudaFreeAsync(w.val, 0);
   if (w.absv) cudaFreeAsync(w.absv, 0);

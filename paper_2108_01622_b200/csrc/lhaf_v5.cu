@@ -61,14 +61,14 @@ __device__ __forceinline__ Pattern pattern_of(const PatDesc &P) {
 // Shared memory of one team (double2 words):
 //   hb    [E+2][NTL]                   band of H (unit subdiagonal), La Budde's q rows after it
 //   u1    union { reduction: cand [2][NW][64] | kb [2][64] | rec [2][NW] | yv [2][NW][2]
-//                            | cmp [NW][4][48]  (compaction, per warp)
+//                            | cmp [NW][4][64]  (compaction, per warp: 8 lanes x up to 8 positions)
 //                 tail:      series scratch 3 (n+2) | La Budde partials [2][NW][2][NTL] }
 //   misc  wv (64 ints) | ww (64 doubles) | beta
 template <int NW>
 struct Shape {
   static constexpr int TS = 32 * NW;
   static constexpr int CAND = 0, KB = CAND + 2 * NW * 64, REC = KB + 2 * 64, YV = REC + 2 * NW,
-                       CMP = YV + 4 * NW, RED_END = CMP + NW * 4 * 48;
+                       CMP = YV + 4 * NW, RED_END = CMP + NW * 4 * 64;
   // band row stride BS = NTL + 1 (odd multiple of 16 B: conflict-free row-strided reads)
   // PREC (double-double tail): q rows, series scratch, level ring and totals twice (hi / lo)
   __host__ __device__ static int u1_words(int E, int NTL, int n, bool prec) {
@@ -418,7 +418,7 @@ __device__ __forceinline__ int2 team_reduce(const PatDesc &P, const Pattern &D, 
     st.colv = (kept || (rho >= E0 && rho < ET)) ? e0 : c0();
     if (!im && rho >= E0 && rho < ET) mg->Z[(rho - E0) * mg->YS] = st.colv;  // z'[label 0]
   }
-  double2 *wbuf = M.u1 + Sh::CMP + warp * 4 * 48;
+  double2 *wbuf = M.u1 + Sh::CMP + warp * 4 * 64;
   if (E != E0) compact<C0, C0, C0>(A, st, wbuf, warp, lane);  // drop the deleted columns
   // ---- a6: phased reduction (the loop-vector columns occupy G positions throughout)
   const int kend = E >= 2 ? E - 2 : 0;

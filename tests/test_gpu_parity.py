@@ -79,6 +79,29 @@ def test_mixed_small(lib, orc, seed):
     assert rel(got, ref) <= tol_for(2 * sum(reps)), (reps, got, ref)
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_mixed_matching_search(lib, orc, seed):
+    # mixed mode 3 (lhaf_rpt_mixed's default): the matching with the least estimated cancellation
+    # among 16 greedy matchings of the doubled pattern (every matching gives the same
+    # lhaf) -- the same value as the oracle's natural pairing and as modes 1 and 2
+    rng = G.rng_for(650 + seed)
+    k = int(rng.integers(3, 7))
+    U = G.haar_unitary(k, rng)
+    A2 = G.lossy_squeezed_A2(U, 0.8, 0.4)
+    g2 = G.complex_gaussian(2 * k, 0.2, rng)
+    reps = G.random_pattern(k, int(rng.integers(4, 10)), rng, max_rep=3)
+    ref = orc.lhaf_mixed(A2, g2, reps)
+    vals = []
+    for mode in (1, 2, 3):
+        job = lib.Job(A2, g2, reps, mixed=mode)
+        job.reset(); job.run()
+        vals.append(job.finalize()[0])
+        job.close()
+    for v in vals:
+        assert rel(v, ref) <= tol_for(2 * sum(reps)), (reps, vals, ref)
+    assert rel(lib.lhaf_rpt_mixed(A2, g2, reps), ref) <= tol_for(2 * sum(reps))
+
+
 def test_cfg3_collision_heavy(lib, orc):
     cfg = G.config(3)
     ref, T, sabs = orc.lhaf_fds(cfg["A"], cfg["gamma"], cfg["reps"])   # 14400 terms, d = 16

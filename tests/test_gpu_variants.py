@@ -38,3 +38,32 @@ def test_variant_block_diagonal(lib, refs, alt):
     got = [complex(a, b) for a, b in json.loads(r.stdout.strip().splitlines()[-1])]
     for g, w in zip(got, refs):
         assert abs(g - w) / abs(w) <= 1e-8, (alt, g, w)
+
+
+def test_v5_zero_weight_deletion_wide(lib):
+    # v5 deletes zero-weight indices per term through a warp's compaction buffer; at a
+    # bordered size E0 >= 49 the tile has 7-8 positions per lane (the buffer row must hold 64).
+    # d = 48: 46 single modes + 2 modes of count 2 (one pair with eta = 2: weight 0 at k = 1);
+    # inclusion/exclusion at N = 48 deletes up to every pair.  Both against the tree (the
+    # oracle-pinned default path, tests/test_gpu_tree.py) on a Haar GBS instance (tanh r = 0.9).
+    import gbs_inputs as G
+    import numpy as np
+    rng = G.rng_for(4848)
+    U = G.haar_unitary(60, rng)
+    B = G.pure_B(U, 0.9)[:48, :48]
+    g = G.complex_gaussian(48, 0.1, rng)
+    reps = np.ones(48, np.int32)
+    reps[[5, 17]] = 2
+    reps[[40, 41]] = 0
+    try:
+        lib.lhaf_set_kernel(6)
+        ref = lib.lhaf_rpt(B, g, reps)
+        ref_et = lib.lhaf_rpt_et(B, g, np.ones(48, np.int32))
+        lib.lhaf_set_kernel(5)
+        got = lib.lhaf_rpt(B, g, reps)
+        got_et = lib.lhaf_rpt_et(B, g, np.ones(48, np.int32))
+    finally:
+        lib.lhaf_set_kernel(0)
+    assert abs(got - ref) / abs(ref) <= 1e-8, (got, ref)
+    # ET's own cancellation (Fig. 5): the two ET codes agree far inside 1e-2
+    assert abs(got_et - ref_et) / abs(ref_et) <= 1e-2, (got_et, ref_et)

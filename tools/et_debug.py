@@ -16,7 +16,8 @@ ga = G.complex_gaussian(m, 0.5, rng); gb = G.complex_gaussian(m, 0.5, rng)
 C = np.block([[A, np.zeros((m, m))], [np.zeros((m, m)), B]]); gc = np.concatenate([ga, gb])
 one = np.ones(m, np.int32)
 ref = oracle.lhaf(A, ga, one, method="et") * oracle.lhaf(B, gb, one, method="et")
-for kern in (6, 5):
+L.lhaf_rpt_et(C, gc, np.ones(N, np.int32)); L.lhaf_rpt(C, gc, np.ones(N, np.int32))  # pool + context warm-up
+for kern in (0, 6, 5):
     L.lhaf_set_kernel(kern)
     t = time.perf_counter(); e = L.lhaf_rpt_et(C, gc, np.ones(N, np.int32)); dt = time.perf_counter() - t
     print(f"N={N} ET kernel {kern}: {e} rel err {abs(e - ref) / abs(ref):.3e}  {dt:.3f} s", flush=True)

@@ -5,7 +5,7 @@ cd $GRAFT_REPO_ROOT
 O=gpurun_out/${1:-prof_tree}
 mkdir -p $O
 timeout 300 python tools/tree_time.py 4 6 512 1 > $O/plain.log 2>&1 || exit 1
-for spec in "tree_pivot_r:30:4" "tree_leaf_r:3:2" "tree_bc_k:30:8" "tree_delta_r:30:2"; do
+for spec in ${PROF_SPECS:-"tree_pivot_s:30:3" "tree_leaf2_r:3:2" "tree_bc_k:30:6"}; do
   IFS=: read name skip cnt <<< "$spec"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$name --launch-skip $skip -c $cnt \
       -o $O/p_$name -f python tools/tree_time.py 4 6 512 1 > $O/ncu_$name.log 2>&1
