@@ -402,7 +402,7 @@ def main():
                 "flops_per_term": own_term,
                 "flops_model": ("tree (variant 6): complex MACs of the level kernels per evaluated leaf x 8"
                                 if job.info.kernel == 6 else "per-term kernel: useful FP64 flops per term"),
-                "kernels": "tree_delta_r/tree_pivot_r/tree_bc_k/tree_leaf_r/tree_reduce_k (+ tree_root_k)"
+                "kernels": "tree_delta_r/tree_pivot_s/tree_bc_k/tree_leaf_r/tree_reduce_k (+ tree_root_k)"
                            if job.info.kernel == 6 else f"sieve (variant {job.info.kernel})",
                 "survey_F_per_term": flops_term,
                 "survey_F_equivalent_tflops": surveyF,
@@ -458,6 +458,20 @@ def main():
     # the n = 40 point of the BASELINE metric: seconds per whole loop hafnian, measured (one
     # GPU's worth of work; rank 0): the collision-free N = 40 instance (2^19 terms at d = 40)
     # and cfg3 (N = 40 with collisions)
+    # mixed state: the kappa-aware matching search of mixed mode 3 (lhaf_rpt_mixed's default) is
+    # a per-lhaf setup cost (candidate sample evaluations); the timed slices use mode 1 (the
+    # same term structure and cost per term -- every candidate has the same multiplicities)
+    search = None
+    if rank == 0 and cfg["mixed"] and world == 1:
+        t0 = time.perf_counter()
+        j1 = L.Job(cfg["A"], cfg["gamma"], reps, mixed=1)
+        t1 = time.perf_counter()
+        j3 = L.Job(cfg["A"], cfg["gamma"], reps, mixed=3)
+        t2 = time.perf_counter()
+        search = {"mode3_setup_s": t2 - t1, "mode1_setup_s": t1 - t0,
+                  "search_s": (t2 - t1) - (t1 - t0), "candidates": 16, "samples_per_candidate": 32,
+                  "matching_eta": list(j3.plan(0).etas())}
+        j1.close(); j3.close()
     n40 = None
     if rank == 0 and world == 1 and not args.no_n40 and args.workload == "cfg4":
         try:
@@ -492,6 +506,7 @@ def main():
             "accuracy": {"kappa": kappa,
                          "pin": "tests/test_gpu_fullsize.py::test_block_diagonal_N60 (P10, P:510; the same default path at d = 60)"},
             "n40": n40,
+            "matching_search": search,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -1027,6 +1027,21 @@ static cudaError_t grow(void **p, size_t &have, size_t need, cudaStream_t st) {
 
 static inline unsigned blocks_for(uint64_t n) { return (unsigned)((n + 127) / 128); }
 
+// Bytes per depth for the run's level buffers (the chunk capacity): bigger chunks mean fewer,
+// larger launches (measured: 512 MB -> 1-2 GB per depth +5-7 % at cfg4, smaller -25 % and
+// worse, profiles/r02/ab_s3_level.txt); default 32 GB / H clamped to [512 MB, 2 GB] so that all
+// depths together stay within 32 GB of the 180 GB.  LHAF_TREE_LEVEL_MB overrides.  The unit
+// plan always uses TreeWork::kLevelBudget: results do not depend on this choice.
+static size_t run_budget(int H) {
+  static const long env_mb = [] {
+    const char *e = getenv("LHAF_TREE_LEVEL_MB");
+    return e ? atol(e) : 0L;
+  }();
+  if (env_mb > 0) return (size_t)env_mb << 20;
+  const size_t b = ((size_t)32 << 30) / (size_t)std::max(1, H);
+  return std::min(std::max(b, TreeWork::kLevelBudget), (size_t)2 << 30);
+}
+
 static int reg_limit() {  // LHAF_TREE_REGL: largest L for the register-array kernels (default 40)
   static const int v = [] {
     const char *e = getenv("LHAF_TREE_REGL");
@@ -1038,11 +1053,12 @@ static int reg_limit() {  // LHAF_TREE_REGL: largest L for the register-array ke
 static size_t bc_smem(int Ep, int b, int L, int G) {
   return ((size_t)bc_smem_parents(G, b) * 2 * Ep + (size_t)G * (2 * Ep + 3)) * L * sizeof(double2);
 }
-// Children per block G and threads per block for tree_bc_k: the choice that maximises a
-// throughput model -- children per block x resident blocks per SM / task rounds per block
-// (each phase's tasks are spread over the block's threads; a round = one task per thread),
-// discounted below 12 resident warps per SM.  LHAF_BC_MODEL=0: the fixed heuristic (128
-// threads, about two tasks each) -- an A/B knob.
+// Children per block G and threads per block for tree_bc_k: the choice that maximises a model
+// of the block's task rounds (each phase's tasks are spread over the block's threads; a round
+// = one task per thread): the lane utilisation of the rounds (idle lanes of a partial round
+// still hold the DFMA pipe) x the saturation of resident warps (14 per SM).  A/B knob
+// LHAF_BC_MODEL: 2 (default) this; 1 children per round-time x blocks; 0 the
+// fixed heuristic (128 threads, about two tasks each).
 static size_t bc_choose(int Ep, int NEc, int b, int L, int &Gbest, int &nbest) {
   static int regs = 0;
   if (!regs) {
@@ -1054,7 +1070,7 @@ static size_t bc_choose(int Ep, int NEc, int b, int L, int &Gbest, int &nbest) {
   const size_t cap = (size_t)LHAF_BC_SMEM_KB << 10;
   static const int model = [] {
     const char *e = getenv("LHAF_BC_MODEL");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
   if (!model) {
     int G = std::max(1, 2 * 128 / (2 * Ep + NEc) + 1);
@@ -1075,7 +1091,11 @@ static size_t bc_choose(int Ep, int NEc, int b, int L, int &Gbest, int &nbest) {
       const int bl_smem = (int)((228u << 10) / (sb + 1024)), bl_reg = 65536 / (regs * nth);
       const int blocks = std::max(1, std::min(std::min(bl_smem, bl_reg), std::min(32, 64 / (nth / 32))));
       const double warps = (double)blocks * nth / 32.0;
-      const double score = (double)blocks * G / r * std::min(1.0, warps / 12.0);
+      // model 1: children per round-time; model 2: lane utilisation of the block's task rounds
+      // (idle lanes of a partial round still occupy the DFMA pipe) x resident-warp saturation
+      const double util = (double)((long)G * 2 * Ep * PB + (long)G * NEc * PC) / (r * nth);
+      const double score = model == 2 ? util * std::min(1.0, warps / 14.0) + 1e-3 * G
+                                      : (double)blocks * G / r * std::min(1.0, warps / 12.0);
       if (score > best) { best = score; Gbest = G; nbest = nth; bestb = sb; }
     }
   return bestb;
@@ -1327,7 +1347,7 @@ cudaError_t tree_run(const JobDev &J, TreeGroup &g, TreeWork &w, uint64_t ub, ui
     R.Pk[k] = k >= g.k_u ? P : 1;
     const int NE = R.E[k] * (R.E[k] + 1) / 2;
     const double nbytes = (double)(NE + 1) * L * 16.0 + 8.0;
-    uint64_t c = (uint64_t)std::max(1.0, (double)TreeWork::kLevelBudget / nbytes);
+    uint64_t c = (uint64_t)std::max(1.0, (double)tree::run_budget(H) / nbytes);
     // never more than the forest has at this depth (small jobs keep small buffers)
     double forest = (double)g.npat;
     for (int l = 0; l < k; ++l) forest *= (double)R.b[l];
