@@ -469,7 +469,7 @@ def main():
         j3 = L.Job(cfg["A"], cfg["gamma"], reps, mixed=3)
         t2 = time.perf_counter()
         search = {"mode3_setup_s": t2 - t1, "mode1_setup_s": t1 - t0,
-                  "search_s": (t2 - t1) - (t1 - t0), "candidates": 16, "samples_per_candidate": 32,
+                  "search_s": (t2 - t1) - (t1 - t0), "candidates": 16, "samples_per_candidate": 8,
                   "matching_eta": list(j3.plan(0).etas())}
         j1.close(); j3.close()
     n40 = None

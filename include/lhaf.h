@@ -110,7 +110,7 @@ lhaf_status lhaf_rpt_batch(const double *A, const double *gamma, int64_t gamma_s
  * 3: every matching gives the same lhaf but not the same cancellation kappa =
  * sum|term| / |lhaf|, which sets the FP64 error; 16 greedy matchings of the
  * doubled pattern (reading C11b; ties broken by seeded relabellings of the modes, the first
- * the identity = mode 1) are each estimated on 32 work units spread over the sieve and the one
+ * the identity = mode 1) are each estimated on 8 work units spread over the sieve and the one
  * with the smallest sum|term| is evaluated (env LHAF_KAPPA_CANDIDATES / LHAF_KAPPA_SAMPLES).
  * Mode 1 (the identity candidate alone) and the natural pairing (i, i+k) x reps_i of
  * P:425-428 (mode 2) are selectable through the job API.  In precise mode the natural pairing

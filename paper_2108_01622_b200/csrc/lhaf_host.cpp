@@ -698,7 +698,7 @@ static int env_int(const char *name, int dflt) {
 static lhaf_status mixed_kappa_plan(const double *A2, const double *g2, const int32_t *reps, int k,
                                     Plan &best, double *best_est) {
   const int C = std::max(1, env_int("LHAF_KAPPA_CANDIDATES", 16));
-  const int S = std::max(1, env_int("LHAF_KAPPA_SAMPLES", 32));
+  const int S = std::max(1, env_int("LHAF_KAPPA_SAMPLES", 8));
   const int k2 = 2 * k;
   std::vector<int32_t> r2(k2);
   for (int i = 0; i < k; ++i) r2[i] = r2[i + k] = reps[i];

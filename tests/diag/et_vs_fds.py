@@ -1,8 +1,8 @@
 """Fig. 5 of the paper on the device path: relative error of the loop hafnian of
 C = A (+) B (block diagonal, random N/2 x N/2 blocks) against lhaf(A) lhaf(B), for the
 finite-difference sieve (lhaf_rpt, FP64; and in precise mode up to --precise-max N) and
-inclusion/exclusion (lhaf_rpt_et: the v5 kernel deletes each term's excluded pairs, so a term
-is reduced at its own size -- P:445), with the reference product from the CPU oracle in x87 long
+inclusion/exclusion (lhaf_rpt_et: on the tree an excluded pair's children copy the parent's
+leading block -- the pair is deleted), with the reference product from the CPU oracle in x87 long
 double (ET tier at N/2).  Device-synchronous wall time per call.  One JSON line per N.
     python tests/diag/et_vs_fds.py [N ...] [--inst=K] [--precise-max=N]"""
 import json
