@@ -433,7 +433,7 @@ def lhaf_set_kernel(variant: int):
 
 
 def lhaf_set_precision(mode: int):
-    """0 = FP64 per term (default), 1 = precise (double-double La Budde + series)."""
+    """0 = FP64 (default: the tree), 1 = precise per-term (double-double La Budde + series, v5)."""
     _check(_lib.lhaf_set_precision(mode))
 
 

@@ -2,11 +2,27 @@
 // double-double accumulation, warp reductions, term decode).  Product code only.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 #include "lhaf_internal.h"
 
 namespace lhaf {
 
 #define LHAF_FULL 0xffffffffu
+
+// Device-side bounds checks of a diagnostic build (-DLHAF_CHECK, tools/build_variant.py; the
+// pool's compute-sanitizer is unavailable): a failed check prints its site and traps.
+#ifdef LHAF_CHECK
+#define LHAF_DCHECK(cond)                                                                   \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("LHAF_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                            \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define LHAF_DCHECK(cond) ((void)0)
+#endif
 
 __device__ __forceinline__ double2 c0() { return make_double2(0.0, 0.0); }
 __device__ __forceinline__ double2 c1() { return make_double2(1.0, 0.0); }

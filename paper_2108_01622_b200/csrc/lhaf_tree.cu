@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(128) tree_delta_r(TStep P, uint64_t p0, uint64
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
   if (i >= np) return;
   const uint64_t ps = p0 + i;
+  LHAF_DCHECK(ps < P.par.cap);
   const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
   const double2 *Kp = P.par.K + (int64_t)ps * NE * L;
   double2 A[LM], B[LM];
@@ -533,6 +534,15 @@ __global__ void __launch_bounds__(PV_THREADS, 2) tree_pivot_s(TStep P) {
   child_of(P, min(i0 + PV_THREADS - 1, P.nc - 1), psl, kh, w);
   child_of(P, i0, psf, kh, w);
   const int NP = (int)(psl - psf) + 1;
+  LHAF_DCHECK(NP >= 1 && NP <= NPM);
+  LHAF_DCHECK(psl < P.par.cap && min(i0 + PV_THREADS, P.nc) <= P.ch.cap);
+#ifdef LHAF_CHECK
+  {
+    unsigned sbytes;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(sbytes));
+    LHAF_DCHECK((size_t)3 * NPM * SP * sizeof(double2) <= sbytes);
+  }
+#endif
   for (int c = threadIdx.x; c < NP * L; c += PV_THREADS) {
     const int p = c / L, s = c - p * L;
     const double2 *Kp = P.par.K + (int64_t)(psf + p) * NE * L;
@@ -632,6 +642,16 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   child_of(P, g0 + G - 1, psl, khl, wl);
   const int NP = (int)(psl - ps0) + 1;
   double2 *cbase = sm + (int64_t)bc_smem_parents(P.G, P.b) * 2 * Ep * L;
+  LHAF_DCHECK(NP >= 1 && NP <= bc_smem_parents(P.G, P.b));
+  LHAF_DCHECK(g0 + G <= P.ch.cap && G >= 1);
+  LHAF_DCHECK(psl < P.par.cap);
+#ifdef LHAF_CHECK
+  {
+    unsigned sbytes;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(sbytes));
+    LHAF_DCHECK((size_t)((int64_t)bc_smem_parents(P.G, P.b) * 2 * Ep * L + (int64_t)P.G * per) * sizeof(double2) <= sbytes);
+  }
+#endif
   // stage: parent rows, then the children's Q
   for (int p = 0; p < NP; ++p) {
     const double2 *Kp = P.par.K + (int64_t)(ps0 + p) * NE * L;
@@ -787,6 +807,7 @@ template <int LM>
 __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
   const uint64_t i = (uint64_t)blockIdx.x * 128 + threadIdx.x;
   if (i >= P.np) return;
+  LHAF_DCHECK(i < P.par.cap);
   const int L = P.L, E = P.E, NE = E * (E + 1) / 2, a = E - 2, b = E - 1;
   const double2 *Kp = P.par.K + (int64_t)i * NE * L;
   const double2 *Kaa = Kp + (int64_t)tri(a, a) * L, *Kbb = Kp + (int64_t)tri(b, b) * L,

@@ -3,7 +3,8 @@ the term's path evaluated with one stage in FP64 and the rest in x87 long double
 all-long-double path (and the oracle term).  Stages: K = the Schur-complement updates
 (T = Q (u, x)^T, K' = K + lam (u T1 + x T2)), P = the pivot series (D, 1/D, log D, Q),
 E = the final exp series and its lam^n coefficient; finer pivot stages: D = the pivot
-determinant D_w, R = 1/D_w, G = log D_w and its sum log c, Q = the 2x2 Q block.
+determinant D_w, R = 1/D_w, G = log D_w and its sum log c, Q = the 2x2 Q block; L = only the
+last eliminated pair's pivot in FP64, U = every pivot but the last.
 usage: python tests/diag/tree_stage_errors.py [cfg] [nsample]"""
 import os
 import sys
@@ -55,9 +56,13 @@ def term_path(C, v, w, n, fp64=""):
     K[d, :d, 0] = -v
     K[:d, d, 0] = -v
     logc = np.zeros(L, LD)
+    last = max([q for q in range(H) if float(w[q]) != 0.0], default=-1)
     for p in range(H):
         a, b = p, p + H
         wp = float(w[p])
+        if "L" in fp64 or "U" in fp64:  # L: only the last pair's pivot in FP64; U: all but the last
+            is_last = p == last
+            tP = np.complex128 if (("L" in fp64 and is_last) or ("U" in fp64 and not is_last)) else LD
         live = [i for i in idx if i != a and i != b]
         if wp == 0.0:
             idx = live
@@ -110,7 +115,7 @@ def main():
     ts = rng.integers(0, T, ns)
     W = np.array([O.decode(int(t), eta)[1] for t in ts], np.int32)
     ref_o = O.fds_terms(C, v, W, n)
-    res = {k: [] for k in ["", "K", "P", "E", "KPE", "D", "R", "G", "Q"]}
+    res = {k: [] for k in ["", "K", "P", "E", "KPE", "L", "U"]}
     for i in range(ns):
         ref = term_path(C, v, W[i], n, "")
         for k in res:

@@ -156,3 +156,4 @@ def test_tree_inclusion_exclusion(lib, orc, seed):
     lib.lhaf_set_kernel(0)
     check(t, ref, sabs, 1e-9)
     assert abs(t - v) <= max(1e-9 * abs(ref), 1e-12 * sabs)
+
