@@ -217,15 +217,17 @@ lhaf_status check_plan_limits(const Plan &P) {
 // Returns false (no halving) when every eta is even.
 bool tree_order(Plan &P) {
   const int H = P.H;
-  std::vector<int> idx(H);
-  for (int h = 0; h < H; ++h) idx[h] = h;
+  // cutoff groups: the batched self-pair (the plan's last pair) is eliminated last -- tree index
+  // 0, the leaf level, where one series serves every count -- and never halves
+  const int batched = P.eta_b >= 0 ? H - 1 : -1;
   int root = -1;
   for (int h = 0; h < H; ++h)
-    if ((P.eta[h] & 1) && (root < 0 || P.eta[h] < P.eta[root])) root = h;
+    if (h != batched && (P.eta[h] & 1) && (root < 0 || P.eta[h] < P.eta[root])) root = h;
   std::vector<int> rest;
   for (int h = 0; h < H; ++h)
-    if (h != root) rest.push_back(h);
+    if (h != root && h != batched) rest.push_back(h);
   std::stable_sort(rest.begin(), rest.end(), [&](int a, int b) { return P.eta[a] > P.eta[b]; });
+  if (batched >= 0) rest.insert(rest.begin(), batched);
   if (root >= 0) rest.push_back(root);
   std::vector<int> p(H), q(H), eta(H);
   for (int t = 0; t < H; ++t) { p[t] = P.p[rest[t]]; q[t] = P.q[rest[t]]; eta[t] = P.eta[rest[t]]; }
@@ -413,12 +415,29 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
     }
   }
 
-  // variant 6 (the prefix-sharing tree) evaluates plain sieves: not the cutoff groups, the
-  // inclusion/exclusion terms or the gamma-batched jobs (their own kernels), not precise mode
+  // variant 6 (the prefix-sharing tree) evaluates plain sieves and inclusion/exclusion: not the
+  // cutoff groups or the gamma-batched jobs (their own kernels), not precise mode.  By default a
+  // job with fewer than LHAF_TREE_MIN_TERMS (65536) evaluated terms runs the per-term v3 kernel
+  // instead: the tree's cost there is the latency of its many small per-level launches (BASELINE
+  // cfg3, 7200 terms: 0.67 ms on the tree, 0.18 ms per term).
   bool use_tree = g_ctx.variant == 6 || (g_ctx.variant == 0 && g_ctx.precision == 0);
   if (plans_in)
     for (const Plan &Pm : *plans_in)
-      if (Pm.eta_b >= 0 || Pm.mg > 0) use_tree = false;
+      if (Pm.mg > 0 || (Pm.eta_b >= 0 && (Pm.n + 1 > 40 || getenv("LHAF_CUTOFF_PER_TERM")))) use_tree = false;
+  if (use_tree && g_ctx.variant == 0) {
+    static const uint64_t min_terms = [] {
+      const char *e = getenv("LHAF_TREE_MIN_TERMS");
+      return e ? strtoull(e, nullptr, 10) : (uint64_t)65536;
+    }();
+    uint64_t tot = 0;
+    for (int b = 0; b < batch && tot < min_terms; ++b) {
+      Plan P;
+      if (plans_in) P = (*plans_in)[b];
+      else if (make_plan(reps + (size_t)b * k, k, mixed, P) != LHAF_OK) break;  // reported below
+      tot += P.et ? P.T : P.T_eval;
+    }
+    if (tot < min_terms) use_tree = false;
+  }
 
   lhaf_job *j = new lhaf_job();
   j->batch = batch;
@@ -540,6 +559,7 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       std::vector<int> key = {D.H, D.n, (D.flags & FLAG_LOOP) ? 1 : 0, (D.flags & (FLAG_FULL | FLAG_ET)) ? 0 : 1,
                               et ? 1 : 0};
       for (int h = 0; h < D.H; ++h) key.push_back(ipool[D.eta_off + h]);
+      if (D.flags & FLAG_CUT) { key.push_back(-1 - b); key.push_back(D.eta_b); }  // one pattern per cutoff group
       size_t gi = 0;
       while (gi < keys.size() && keys[gi] != key) ++gi;
       if (gi == keys.size()) {
@@ -547,7 +567,8 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
         TreeGroup g;
         g.H = D.H; g.n = D.n; g.bord = key[2]; g.halve = key[3];
         g.wmul = key[4] ? 1 : 2;  // inclusion/exclusion: w = eta - k; sieve: eta - 2k
-        g.eta.assign(key.begin() + 5, key.end());
+        g.eta.assign(key.begin() + 5, key.begin() + 5 + D.H);
+        if (D.flags & FLAG_CUT) { g.cut_eb = D.eta_b; g.nf = D.n - D.eta_b; }
         j->groups.push_back(g);
       }
       j->groups[gi].pats.push_back(b);
@@ -556,15 +577,16 @@ static lhaf_status job_create_impl(const double *A, const double *gamma, int64_t
       g.npat = (int)g.pats.size();
       tree_plan_group(g, 65536);
       g.unit_base = unit;
+      g.part_base = part;
       for (int32_t pb : g.pats) {
         PatDesc &D = j->descs[pb];
         D.unit_begin = unit;
         D.units = g.units_pp;
         D.chunk = D.T_eval / g.units_pp;  // leaves per unit
-        D.part_base = (int64_t)unit;
+        D.part_base = (int64_t)part;
         unit += g.units_pp;
+        part += g.units_pp * (uint64_t)(g.cut_eb >= 0 ? g.cut_eb + 1 : 1);
       }
-      part = unit;
       j->tree_flops = 8.0 * tree_cmacs_per_term(g);
     }
   }
@@ -1015,7 +1037,7 @@ static lhaf_status cutoff_impl(const double *A, const double *gamma, const int32
   Plan Pf;
   lhaf_status s = make_plan(rf.data(), k, 0, Pf);
   if (s != LHAF_OK) return s;
-  const bool shared = n_cut <= 63 && !getenv("LHAF_CUTOFF_SEPARATE") && g_ctx.variant == 0;
+  const bool shared = n_cut <= 63 && !getenv("LHAF_CUTOFF_SEPARATE") && (g_ctx.variant == 0 || g_ctx.variant == 6);
   std::vector<Plan> groups;
   int n_f[2] = {0, 0}, gidx[2] = {-1, -1};
   if (shared) {
@@ -1083,6 +1105,7 @@ static lhaf_status cutoff_impl(const double *A, const double *gamma, const int32
     PatDesc &D = vd[c];
     memset(&D, 0, sizeof D);
     D.d = (Pf.N + c == 0) ? 0 : 2;
+    D.flags = G.flags & FLAG_FULL;  // the tree evaluates every term when no fixed pair can halve
     D.n = n_f[c & 1] + m;
     D.unit_begin = (uint64_t)G.part_base + (uint64_t)m * G.units;
     D.units = G.units;
@@ -1096,7 +1119,8 @@ static lhaf_status cutoff_impl(const double *A, const double *gamma, const int32
   if (e == cudaSuccess) e = dmalloc(&d_ab, (n_cut + 1) * sizeof(double));
   if (e == cudaSuccess) e = cudaMemset(j->d_partials, 0, std::max<uint64_t>(1, j->parts) * sizeof(Partial));
   if (e == cudaSuccess)
-    e = launch_sieve_cut_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, 0, j->units, g_ctx.num_sms, 0);
+    e = (j->variant == 6) ? run_sieve(j, 0, j->units, 0)  // the batched pair at the tree's leaves
+                          : launch_sieve_cut_v3(j->dev(), j->e_max, j->ntl_max, j->n_max, 0, j->units, g_ctx.num_sms, 0);
   if (e == cudaSuccess) {
     JobDev J = j->dev();
     J.descs = d_vd;

@@ -123,6 +123,10 @@ struct TLevel {   // the nodes of one depth: K[(node * NE + e) * L + s], logc[no
 struct TreeGroup {            // patterns that share one tree shape
   int H = 0, n = 0, bord = 0, halve = 1, k_u = 0, npat = 0;
   int wmul = 2;               // digit k -> weight eta - wmul k (2: the sieve; 1: inclusion/exclusion)
+  int cut_eb = -1;            // >= 0: cutoff group (FLAG_CUT, one pattern): the leaf pair is the
+                              // batched self-pair, weights w_b = (eta - 2k) / 2 in [-eta_b, eta_b]
+  int nf = 0;                 // cutoff group: the fixed pairs' degree (count 2m + p at nf + m)
+  uint64_t part_base = 0;     // cutoff group: first partial (count m at part_base + m * units_pp)
   std::vector<int> eta;       // tree order: pair H-1 is eliminated first (depth 0)
   std::vector<int32_t> pats;  // job pattern indices, in unit order
   int32_t *d_pats = nullptr;

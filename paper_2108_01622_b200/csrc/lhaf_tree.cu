@@ -797,6 +797,8 @@ struct TLeaf {
   double2 *S;      // scratch [np][9][L]
   double2 *val;    // [np]: sum over the node's leaves of sign * prod C * g
   double *absv;    // [np]: the same sum of |.|
+  int cut_eb, nf;  // cutoff group (cut_eb >= 0): per count m, val / absv at [m * vstride + node]
+  uint64_t vstride;
 };
 
 // The last pair of every node, both (all) digits; the node-level products shared by the leaves:
@@ -841,9 +843,13 @@ __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
   const double coef = P.par.coef[i];
   double2 vsum = c0();
   double asum = 0.0;
+  const bool cut = P.cut_eb >= 0;
+  if (cut)
+    for (int m = 0; m <= P.cut_eb; ++m) { P.val[m * P.vstride + i] = c0(); P.absv[m * P.vstride + i] = 0.0; }
 #pragma unroll 1
   for (int d = 0; d < P.b; ++d) {
-    const int kh = P.dmin + d, w = P.eta - P.wmul * kh;
+    // cutoff groups: the leaf pair is the batched self-pair, weight w_b = (eta - 2 k) / 2
+    const int kh = P.dmin + d, w = cut ? (P.eta - P.wmul * kh) / 2 : P.eta - P.wmul * kh;
     const double wd = (double)w, w2 = wd * wd;
     // phases sharing one recursion instance: 0: R = 1/D; 1: t log D; 2: exp(phi)
 #pragma unroll 1
@@ -882,6 +888,24 @@ __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
         }
       }
     }
+    if (cut) {
+      // every count 2m + p with m >= |w_b|, m = w_b (mod 2): (-1)^{k_b} C(m, k_b) [lam^{nf + m}] F,
+      // k_b = (m - w_b) / 2 (App. B.5)
+#pragma unroll 1
+      for (int m = abs(w); m <= P.cut_eb; m += 2) {
+        const int deg = P.nf + m;
+        double2 g = c0();
+#pragma unroll
+        for (int t = 0; t < LM; ++t)
+          if (t == deg) g = B[t];
+        const int kb = (m - w) / 2;
+        const double cb = binom_d(m, kb), f = coef * ((kb & 1) ? -cb : cb);
+        double2 *vp = P.val + m * P.vstride + i;
+        *vp = make_double2(fma(f, g.x, vp->x), fma(f, g.y, vp->y));
+        P.absv[m * P.vstride + i] += fabs(f) * hypot(g.x, g.y);
+      }
+      continue;
+    }
     double2 g = c0();
 #pragma unroll
     for (int t = 0; t < LM; ++t)
@@ -891,6 +915,7 @@ __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
     vsum.y = fma(f, g.y, vsum.y);
     asum += fabs(f) * hypot(g.x, g.y);
   }
+  if (cut) return;
   P.val[i] = vsum;
   P.absv[i] = asum;
 }
@@ -1166,8 +1191,24 @@ struct Runner {
     P.S = (double2 *)w.scratch;
     P.val = (double2 *)w.val;
     P.absv = (double *)w.absv;
+    P.cut_eb = g.cut_eb; P.nf = g.nf; P.vstride = cap[k];
     ++lhaf::g_launches;
     const int rl = reg_limit();
+    if (g.cut_eb >= 0) {  // cutoff group: register-array leaf only (the host keeps L <= 40 here)
+      const uint64_t per = Pk[k], units = cnt / per;
+      if (L <= 16) tree_leaf_r<16><<<blocks_for(cnt), 128, 0, st>>>(P);
+      else if (L <= 24) tree_leaf_r<24><<<blocks_for(cnt), 128, 0, st>>>(P);
+      else if (L <= 32) tree_leaf_r<32><<<blocks_for(cnt), 128, 0, st>>>(P);
+      else tree_leaf_r<40><<<blocks_for(cnt), 128, 0, st>>>(P);
+      cudaError_t e = cudaGetLastError();
+      for (int m = 0; m <= g.cut_eb && e == cudaSuccess; ++m) {
+        ++lhaf::g_launches;
+        tree_reduce_k<<<(unsigned)units, 256, 0, st>>>(P.val + m * cap[k], P.absv + m * cap[k], per,
+                                                       g.part_base + (uint64_t)m * g.units_pp + gs / per, J.partials);
+        e = cudaGetLastError();
+      }
+      return e;
+    }
     if (L <= 16 && L <= rl) tree_leaf_r<16><<<blocks_for(cnt), 128, 0, st>>>(P);
     else if (L <= 24 && L <= rl) tree_leaf_r<24><<<blocks_for(cnt), 128, 0, st>>>(P);
     else if (L <= 32 && L <= rl) tree_leaf_r<32><<<blocks_for(cnt), 128, 0, st>>>(P);
@@ -1387,8 +1428,9 @@ cudaError_t tree_run(const JobDev &J, TreeGroup &g, TreeWork &w, uint64_t ub, ui
   cudaError_t e = cudaSuccess;
   for (int k = 0; k < H && e == cudaSuccess; ++k) e = R.level_alloc(k);
   if (e == cudaSuccess) e = tree::grow(&w.scratch, w.scratch_bytes, scratch * sizeof(double2), st);
-  if (e == cudaSuccess) e = tree::grow(&w.val, w.val_bytes, (size_t)R.cap[H - 1] * sizeof(double2), st);
-  if (e == cudaSuccess) e = tree::grow(&w.absv, w.abs_bytes, (size_t)R.cap[H - 1] * sizeof(double), st);
+  const size_t nvals = (size_t)R.cap[H - 1] * (size_t)(g.cut_eb >= 0 ? g.cut_eb + 1 : 1);
+  if (e == cudaSuccess) e = tree::grow(&w.val, w.val_bytes, nvals * sizeof(double2), st);
+  if (e == cudaSuccess) e = tree::grow(&w.absv, w.abs_bytes, nvals * sizeof(double), st);
   if (e != cudaSuccess) return e;
   return R.run();
 }

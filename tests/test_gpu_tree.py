@@ -10,6 +10,8 @@ patterns fall into several tree shapes, and unit ranges (bit-identical results f
 Tolerances: the north_star's 1e-10 for N <= 24 (relative), absolute against sum|term| where the
 exact value is 0 (reading C18).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -157,3 +159,40 @@ def test_tree_inclusion_exclusion(lib, orc, seed):
     check(t, ref, sabs, 1e-9)
     assert abs(t - v) <= max(1e-9 * abs(ref), 1e-12 * sabs)
 
+
+
+@pytest.mark.parametrize("fixed,mode,n_cut,loops", [
+    ([1, 2, 0, 1, 0, 1, 0, 0], 2, 9, True),     # odd N_f: the leftover photon pairs with mode 2
+    ([2, 0, 1, 1, 0, 0, 2, 0], 5, 12, True),    # even N_f: the odd counts get a phantom pair
+    ([1, 1, 0, 1, 0, 0, 0, 1], 0, 10, False),   # no loops: odd totals vanish
+    ([0] * 8, 3, 7, True),                      # nothing fixed: single-mode counts 0..7
+    ([2, 2, 0, 2, 0, 0, 0, 0], 1, 8, True),     # every fixed eta even: no halving on the tree
+])
+def test_tree_cutoff_batched(lib, orc, fixed, mode, n_cut, loops):
+    # App. B.5 on the tree: the batched self-pair is the leaf level, one series per
+    # (fixed-pair prefix, w_b) serves every count 2m + p; against the oracle per count and the
+    # per-term shared evaluation (v3)
+    rng = G.rng_for(5330 + n_cut)
+    k = 8
+    A = G.pure_B(G.haar_unitary(k, rng), 0.75)
+    g = G.complex_gaussian(k, 0.35, rng) if loops else np.zeros(k, complex)
+    fixed = np.array(fixed, np.int32)
+    try:
+        lib.lhaf_set_kernel(6)
+        vals = lib.lhaf_rpt_cutoff(A, g, fixed, mode, n_cut)
+    finally:
+        lib.lhaf_set_kernel(0)
+    os.environ["LHAF_CUTOFF_PER_TERM"] = "1"
+    try:
+        per_term = lib.lhaf_rpt_cutoff(A, g, fixed, mode, n_cut)
+    finally:
+        del os.environ["LHAF_CUTOFF_PER_TERM"]
+    for c in range(n_cut + 1):
+        reps = fixed.copy()
+        reps[mode] = c
+        ref = orc.lhaf(A, g, reps)
+        if abs(ref) == 0.0:
+            assert abs(vals[c]) <= 1e-13 * max(1.0, max(abs(x) for x in per_term)), (c, vals[c])
+            continue
+        assert rel(vals[c], ref) <= 1e-10, (c, vals[c], ref)
+        assert rel(vals[c], per_term[c]) <= 1e-11, (c, vals[c], per_term[c])
