@@ -127,9 +127,12 @@ lhaf_status lhaf_rpt_mixed(const double *A2, const double *gamma2, const int32_t
  * and the batched mode becomes a self-pair (mode, mode) with eta_b = floor((n_cut - p) / 2) in
  * two groups by the parity p of its count (odd counts add one single-photon pair: with the
  * fixed part's leftover photon, or with the phantom); every term (fixed-pair term, w_b in
- * [-eta_b, eta_b]) is ONE Hessenberg reduction + La Budde + series to degree n_f + eta_b whose
- * coefficients serve every count 2m + p with m >= |w_b|, m = w_b (mod 2), weighted by
- * (-1)^k C(m, k), k = (m - w_b) / 2 (sieve_cut_v3).  One sieve launch, one finalize.
+ * [-eta_b, eta_b]) is ONE series to degree n_f + eta_b whose coefficients serve every count
+ * 2m + p with m >= |w_b|, m = w_b (mod 2), weighted by (-1)^k C(m, k), k = (m - w_b) / 2.
+ * Default (series length n_f + eta_b + 1 <= 40, >= 65536 terms): the prefix-sharing tree with
+ * the batched self-pair as its leaf level (every prefix of fixed pairs shared); otherwise, or
+ * with LHAF_CUTOFF_PER_TERM set, one Hessenberg reduction + La Budde per term (sieve_cut_v3).
+ * One sieve evaluation, one finalize.
  * n_cut = 64, or LHAF_CUTOFF_SEPARATE set in the environment, evaluates the n_cut + 1 patterns
  * as independent sieves in one batch job instead (same values up to rounding: both orders
  * carry the sieve's cancellation, ~kappa * eps per count).  Errors as lhaf_rpt_batch, plus
