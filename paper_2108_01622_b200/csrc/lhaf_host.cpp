@@ -1147,8 +1147,15 @@ lhaf_status lhaf_rpt_multigamma(const double *A, const double *gammas, int32_t n
   lhaf_status s = make_plan(reps, k, 0, plans[0]);
   if (s != LHAF_OK) return s;
   const Plan &P0 = plans[0];
+  // the shared per-term reduction (v5 FLAG_MG) against G patterns in one tree forest: on the
+  // tree (FP64, >= 65536 terms per loop vector) the separate evaluation is faster -- d = 48,
+  // G = 16: 2.7 s against 8.2 s (DESIGN.md §9 row 2) -- so the shared path serves the per-term
+  // regime (small patterns) and explicit requests (LHAF_MULTIGAMMA_SHARED, kernel 5)
+  const bool tree_regime = g_ctx.variant == 0 && g_ctx.precision == 0 && P0.T_eval >= 65536 &&
+                           !getenv("LHAF_MULTIGAMMA_SHARED");
   const bool shared = P0.H > 0 && P0.d + ngamma <= 64 && ngamma <= LHAF_MAX_GAMMA &&
-                      g_ctx.variant == 0 && g_ctx.precision == 0 && !getenv("LHAF_MULTIGAMMA_SEPARATE");
+                      (g_ctx.variant == 0 || g_ctx.variant == 5) && g_ctx.precision == 0 && !tree_regime &&
+                      !getenv("LHAF_MULTIGAMMA_SEPARATE");
   if (!shared) {
     // the pattern once per loop vector in one batch job (G independent sieves)
     std::vector<int32_t> r((size_t)ngamma * k);
