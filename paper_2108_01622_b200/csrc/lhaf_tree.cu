@@ -625,6 +625,12 @@ __global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
 #ifndef LHAF_BC_SMEM_KB
 #define LHAF_BC_SMEM_KB 72
 #endif
+// Task order inside a phase: 1 = part-major (the lanes of a warp work on the same pair of output
+// blocks, so the windowed loops of a warp have one trip count); 0 = part fastest (lanes 2i, 2i+1
+// take the short and the long pair: the warp runs max(trip counts) per block, ~25 % idle lanes).
+#ifndef LHAF_BC_ORDER
+#define LHAF_BC_ORDER 1
+#endif
 constexpr int BC_THREADS = LHAF_BC_THREADS;
 // parents a group of G consecutive children can span (b children per parent)
 __host__ __device__ __forceinline__ int bc_smem_parents(int G, int b) { return min(G, (G - 1) / b + 2); }
@@ -672,8 +678,9 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   // tasks are split by output blocks, paired (p, nb - 1 - p) so that every task does about the
   // same work (the products are triangular): PB parts per series
   const int nbB = (Lo + TB - 1) / TB, PB = (nbB + 1) / 2;
-  for (int task = tid; task < G * 2 * Ep * PB; task += nth) {
-    const int part = task % PB, tk = task / PB;
+  const int NT1 = G * 2 * Ep;
+  for (int task = tid; task < NT1 * PB; task += nth) {
+    const int part = LHAF_BC_ORDER ? task / NT1 : task % PB, tk = LHAF_BC_ORDER ? task - part * NT1 : task / PB;
     const int g = tk / (2 * Ep), r = tk - g * 2 * Ep, j = r >> 1, which = r & 1;
     uint64_t ps; int kh, w;
     child_of(P, g0 + g, ps, kh, w);
@@ -700,8 +707,9 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   }
   __syncthreads();
   const int nbC = (L + TB - 1) / TB, PC = (nbC + 1) / 2;
-  for (int task = tid; task < G * NEc * PC; task += nth) {
-    const int part = task % PC, tk = task / PC;
+  const int NT2 = G * NEc;
+  for (int task = tid; task < NT2 * PC; task += nth) {
+    const int part = LHAF_BC_ORDER ? task / NT2 : task % PC, tk = LHAF_BC_ORDER ? task - part * NT2 : task / PC;
     const int g = tk / NEc, e = tk - g * NEc;
     int ii = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
     while (tri(ii + 1, 0) <= e) ++ii;

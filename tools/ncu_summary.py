@@ -49,5 +49,10 @@ for r in data:
         "dram_read_bytes": get(r, "dram__bytes_read.sum", scaled=True),
         "dram_write_bytes": get(r, "dram__bytes_write.sum", scaled=True),
         "top_stalls_per_issue": top,
+        "threads_per_inst": {h: get(r, h) for h in hdr if "per_inst_executed" in h},
+        "occupancy_limits": {h: get(r, h) for h in hdr if h.startswith("launch__occupancy_limit")},
+        "smem_dynamic_bytes": get(r, "launch__shared_mem_per_block_dynamic", scaled=True),
+        "inst_executed": get(r, "smsp__inst_executed.sum"),
+        "shared_bank_conflicts": {h: get(r, h) for h in hdr if "bank_conflicts" in h and "shared" in h},
     })
 print(json.dumps(out if len(out) > 1 else out[0], indent=1))
