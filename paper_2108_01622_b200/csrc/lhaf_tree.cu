@@ -73,6 +73,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef LHAF_TWOPASS
 #define LHAF_TWOPASS 1
 #endif
+#ifndef LHAF_RS_PREFETCH
+#define LHAF_RS_PREFETCH 0
+#endif
 __device__ __forceinline__ void cfma_row(double2 (&acc)[TB], double2 av, const double2 (&w)[TB], const int RHO) {
   if (!LHAF_TWOPASS) {
 #pragma unroll
@@ -137,6 +140,74 @@ __device__ __forceinline__ void conv_acc(double2 (&acc)[TB], int t0, int sh, SR 
       for (int j = 1; j < TB; ++j) {
         if (j >= jlo && j <= jhi) {
           const double2 av = ap[(int64_t)j * a.st];
+#pragma unroll
+          for (int k = j; k < TB; ++k) acc[k] = cfma(av, bq[k - j], acc[k]);
+        }
+      }
+    }
+  }
+}
+
+// conv_acc for unit-stride operands in shared memory, written for ONE inlined instance per kernel
+// (tree_bc_k): full chunks of TB steps run without per-step guards, so ptxas hoists the two
+// shared-memory loads of a step over the FMAs of the steps before it (with a guard per step a
+// third of the loop's cycles were short-scoreboard stalls on the first FMA after the loads,
+// profiles/r02/s5/ncu_bc_order1.json); the last nsteps mod TB steps leave by one forward branch.
+__device__ __forceinline__ void conv_acc1(double2 (&acc)[TB], int t0, int sh, const double2 *a, int La,
+                                          const double2 *b, int Lb) {
+  const int base = t0 - sh;
+  const int s_lo = max(0, base - (Lb - 1));
+  const int s_hi = min(La - 1, base + TB - 1);
+  if (s_lo > s_hi) return;
+  const int s_top = min(s_hi, base);
+  if (s_lo <= s_top) {
+    const int Q0 = base - s_lo;
+    double2 w[TB];
+#pragma unroll
+    for (int k = 0; k < TB; ++k) {
+      const int q = Q0 + k;
+      w[k] = (q < Lb) ? b[q] : c0();
+    }
+    const int nsteps = s_top - s_lo + 1;
+    const double2 *ap = a + s_lo, *bp = b + Q0;
+    int r0 = 0;
+    for (; r0 + TB <= nsteps; r0 += TB) {
+#pragma unroll
+      for (int rho = 0; rho < TB; ++rho) {
+        w[(TB - rho) % TB] = bp[-(r0 + rho)];  // step 0 reloads w[0] = b[Q0]
+        cfma_row(acc, ap[r0 + rho], w, rho);
+      }
+    }
+    const int rem = nsteps - r0;
+#pragma unroll
+    for (int rho = 0; rho < TB - 1; ++rho) {
+      if (rho >= rem) break;
+      w[(TB - rho) % TB] = bp[-(r0 + rho)];
+      cfma_row(acc, ap[r0 + rho], w, rho);
+    }
+  }
+  {  // triangle
+    const int jlo = max(1, -base), jhi = s_hi - base;
+    if (jlo == 1 && jhi == TB - 1 && Lb >= TB - 1) {
+      double2 bq[TB - 1];
+#pragma unroll
+      for (int q = 0; q < TB - 1; ++q) bq[q] = b[q];
+      const double2 *ap = a + base;
+#pragma unroll
+      for (int j = 1; j < TB; ++j) {
+        const double2 av = ap[j];
+#pragma unroll
+        for (int k = j; k < TB; ++k) acc[k] = cfma(av, bq[k - j], acc[k]);
+      }
+    } else if (jlo <= jhi) {
+      double2 bq[TB - 1];
+#pragma unroll
+      for (int q = 0; q < TB - 1; ++q) bq[q] = (q < Lb && q <= TB - 1 - jlo) ? b[q] : c0();
+      const double2 *ap = a + base;
+#pragma unroll
+      for (int j = 1; j < TB; ++j) {
+        if (j >= jlo && j <= jhi) {
+          const double2 av = ap[j];
 #pragma unroll
           for (int k = j; k < TB; ++k) acc[k] = cfma(av, bq[k - j], acc[k]);
         }
@@ -411,6 +482,28 @@ __device__ __forceinline__ void rrec(double2 (&X)[LM], const double2 (&P)[LM], i
 template <int LM>
 __device__ __forceinline__ void rs_op(double2 (&acc)[LM], const double2 *__restrict__ a, const double2 (&B)[LM], int L,
                                       double sgn) {
+#if LHAF_RS_PREFETCH
+  // a[s + 1] (and a[s + 2]) are requested before the FMAs of step s: a is a per-thread series in
+  // HBM / L2 and every step began with a long-scoreboard stall on its own load (tree_leaf_r)
+  double2 n0 = a[0];
+#if LHAF_RS_PREFETCH > 1
+  double2 n1 = a[min(1, L - 1)];
+#endif
+#pragma unroll
+  for (int s = 0; s < LM; ++s) {
+    if (s < L) {
+      const double2 av = cscale(n0, sgn);
+#if LHAF_RS_PREFETCH > 1
+      n0 = n1;
+      n1 = a[min(s + 2, L - 1)];
+#else
+      n0 = a[min(s + 1, L - 1)];
+#endif
+#pragma unroll
+      for (int q = 0; q + s < LM; ++q) acc[q + s] = cfma(av, B[q], acc[q + s]);
+    }
+  }
+#else
 #pragma unroll
   for (int s = 0; s < LM; ++s) {
     if (s < L) {
@@ -419,6 +512,7 @@ __device__ __forceinline__ void rs_op(double2 (&acc)[LM], const double2 *__restr
       for (int q = 0; q + s < LM; ++q) acc[q + s] = cfma(av, B[q], acc[q + s]);
     }
   }
+#endif
 }
 
 // ================================================================ kernels
@@ -620,7 +714,7 @@ __global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
 #define LHAF_BC_THREADS 128
 #endif
 #ifndef LHAF_BC_MINB
-#define LHAF_BC_MINB 3
+#define LHAF_BC_MINB 4
 #endif
 #ifndef LHAF_BC_SMEM_KB
 #define LHAF_BC_SMEM_KB 72
@@ -630,6 +724,9 @@ __global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
 // take the short and the long pair: the warp runs max(trip counts) per block, ~25 % idle lanes).
 #ifndef LHAF_BC_ORDER
 #define LHAF_BC_ORDER 1
+#endif
+#ifndef LHAF_BC_UNIFIED
+#define LHAF_BC_UNIFIED 1
 #endif
 constexpr int BC_THREADS = LHAF_BC_THREADS;
 // parents a group of G consecutive children can span (b children per parent)
@@ -674,6 +771,79 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
   }
   cp_async_wait_all();
   __syncthreads();
+#if LHAF_BC_UNIFIED
+  // Both phases -- T = Q (u, x)^T into shared memory, then K' = K + lam (u T1 + x T2) -- run through
+  // one task loop with one inlined conv_acc1 (the two products of a task in a rolled loop): the
+  // kernel's code is a quarter of the four-instance version (tree_bc_k was 54 KB of SASS and
+  // stalled on instruction fetch).  Tasks are output blocks paired (p, nb - 1 - p) so that every
+  // task does about the same work; part-major order (LHAF_BC_ORDER).
+  const int Lo = L - 1;
+  const int nbB = (Lo + TB - 1) / TB, PB = (nbB + 1) / 2;
+  const int nbC = (L + TB - 1) / TB, PC = (nbC + 1) / 2;
+#pragma unroll 1
+  for (int phase = 0; phase < 2; ++phase) {
+    const int NT = phase ? G * NEc : G * 2 * Ep, NPt = phase ? PC : PB, nb = phase ? nbC : nbB;
+    const int Lout = phase ? L : Lo;
+#pragma unroll 1
+    for (int task = tid; task < NT * NPt; task += nth) {
+      const int part = LHAF_BC_ORDER ? task / NT : task % NPt, tk = LHAF_BC_ORDER ? task - part * NT : task / NPt;
+      int g, a0o, a1o, b0o, b1o, oo = 0;   // operand / output offsets in sm (double2 units)
+      const double2 *K = nullptr;
+      double2 *out = nullptr;
+      uint64_t ps; int kh, w;
+      if (!phase) {
+        g = tk / (2 * Ep);
+        const int r = tk - g * 2 * Ep, j = r >> 1, which = r & 1;
+        child_of(P, g0 + g, ps, kh, w);
+        if (w == 0) continue;  // deleted pair: the child is the parent's leading block
+        const int Uo = (int)(ps - ps0) * 2 * Ep * L, Co = (int)(cbase - sm) + g * per;
+        // T1 = q11 u + q12 x ; T2 = q12 u + q22 x
+        a0o = Co + (which ? L : 0); a1o = Co + (which ? 2 * L : L);
+        b0o = Uo + j * L; b1o = Uo + Ep * L + j * L;
+        oo = Co + 3 * L + which * Ep * L + j * L;
+      } else {
+        g = tk / NEc;
+        const int e = tk - g * NEc;
+        int ii = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+        while (tri(ii + 1, 0) <= e) ++ii;
+        while (tri(ii, 0) > e) --ii;
+        const int jj = e - tri(ii, 0);
+        child_of(P, g0 + g, ps, kh, w);
+        const int Uo = (int)(ps - ps0) * 2 * Ep * L, Co = (int)(cbase - sm) + g * per;
+        a0o = Uo + ii * L; a1o = Uo + Ep * L + ii * L;
+        b0o = Co + 3 * L + jj * L; b1o = Co + 3 * L + Ep * L + jj * L;
+        K = P.par.K + ((int64_t)ps * NE + e) * L;
+        out = P.ch.K + ((int64_t)(g0 + g) * NEc + e) * L;
+      }
+#pragma unroll 1
+      for (int bi = 0; bi < 2; ++bi) {
+        const int blk = bi ? nb - 1 - part : part;
+        if (bi && blk == part) break;
+        const int t0 = blk * TB;
+        if (phase && w == 0) {
+          for (int t = t0; t < t0 + TB && t < L; ++t) out[t] = K[t];
+          continue;
+        }
+        double2 acc[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) acc[k] = (phase && t0 + k < L) ? K[t0 + k] : c0();
+#pragma unroll 1
+        for (int op = 0; op < 2; ++op) conv_acc1(acc, t0, phase, sm + (op ? a1o : a0o), Lo, sm + (op ? b1o : b0o), Lo);
+        if (phase) {
+#pragma unroll
+          for (int k = 0; k < TB; ++k)
+            if (t0 + k < Lout) out[t0 + k] = acc[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < TB; ++k)
+            if (t0 + k < Lout) sm[oo + t0 + k] = acc[k];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+#else
   const int Lo = L - 1;
   // tasks are split by output blocks, paired (p, nb - 1 - p) so that every task does about the
   // same work (the products are triangular): PB parts per series
@@ -740,6 +910,7 @@ __global__ void __launch_bounds__(BC_THREADS, LHAF_BC_MINB) tree_bc_k(TStep P) {
     }
   }
 }
+#endif
 
 // fallback when a child group's rows do not fit shared memory: T in HBM, then the update
 __global__ void __launch_bounds__(128) tree_tmat_g(TStep P) {
