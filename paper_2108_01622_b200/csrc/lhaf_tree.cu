@@ -76,6 +76,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef LHAF_RS_PREFETCH
 #define LHAF_RS_PREFETCH 0
 #endif
+#ifndef LHAF_LEAF_PREFETCH
+#define LHAF_LEAF_PREFETCH 0
+#endif
 __device__ __forceinline__ void cfma_row(double2 (&acc)[TB], double2 av, const double2 (&w)[TB], const int RHO) {
   if (!LHAF_TWOPASS) {
 #pragma unroll
@@ -368,6 +371,15 @@ __device__ __forceinline__ void rstore(double2 *p, const double2 (&A)[LM], int L
 #pragma unroll
   for (int t = 0; t < LM; ++t)
     if (t < L) p[t] = A[t];
+}
+// Request a per-thread series (global memory) into L1: one prefetch per 32-byte sector, no
+// scoreboard.  The streamed operand of the product that follows then hits L1 instead of taking one
+// L2 round trip per sector, serialised by the product's steps (tree_leaf_r: long-scoreboard stalls).
+__device__ __forceinline__ void rprefetch(const double2 *p, int L) {
+#if LHAF_LEAF_PREFETCH
+  for (int s = 0; s < L; s += 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + s));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p + L - 1));
+#endif
 }
 // acc[t] (+/-)= sum_{s + q + SH = t} a[s] B[q]  for t < L  (a streamed, B in registers).
 // Entries t >= L are never read: computing them (zero-padded operands) is harmless, so the
@@ -1010,10 +1022,11 @@ __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
 #pragma unroll 1
   for (int op = 0; op < nops; ++op) {
     const double2 *ld = (op == 0) ? Kaa : (op == 1 || op == 4) ? u : (op == 2 || op == 6) ? x : nullptr;
-    if (ld) rload(B, ld, L);
-    if (op == 1 || op == 3 || op == 5 || op == 7) rz(A);
     const double2 *src = (op == 0 || op == 1) ? Kbb : (op == 2 || op == 4) ? Kab : (op == 3) ? Kaa
                        : (op == 5) ? S1 : (op == 6) ? S2 : u;
+    rprefetch(src, L);
+    if (ld) rload(B, ld, L);
+    if (op == 1 || op == 3 || op == 5 || op == 7) rz(A);
     const double sg = (op == 0 || op == 2 || op == 4) ? -1.0 : 1.0;
     rs_op(A, src, B, L, sg);
     double2 *st = (op == 0) ? S0 : (op == 2 || op == 6) ? S1 : (op == 4 || op == 7) ? S2 : nullptr;
@@ -1046,6 +1059,7 @@ __global__ void __launch_bounds__(128) tree_leaf_r(TLeaf P) {
               S3[t] = nv;
             }
           rz(A);
+          rprefetch(S3, L);
           rs_op(A, S3, B, L, 1.0);
           rstore(S3, A, L);
         }
