@@ -30,7 +30,7 @@ tot_t = sum(p["gpu__time_duration.sum"] for p in per.values())
 out = {"label": sys.argv[3], "terms": terms, "dram_read_bytes": tot_r, "dram_write_bytes": tot_w,
        "bytes_per_term": (tot_r + tot_w) / terms, "kernel_time_s": tot_t,
        "kernels": {k: {"launches": cnt[k], "time_s": p["gpu__time_duration.sum"],
-                       "share": p["gpu__time_duration.sum"] / tot_t,
+                       "share": (p["gpu__time_duration.sum"] / tot_t) if tot_t else None,
                        "dram_bytes": p["dram__bytes_read.sum"] + p["dram__bytes_write.sum"]}
                    for k, p in sorted(per.items(), key=lambda x: -x[1]["gpu__time_duration.sum"])}}
 print(json.dumps(out, indent=1))
