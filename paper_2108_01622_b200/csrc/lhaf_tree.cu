@@ -79,6 +79,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef LHAF_LEAF_PREFETCH
 #define LHAF_LEAF_PREFETCH 0
 #endif
+#ifndef LHAF_PIVOT_TWO
+#define LHAF_PIVOT_TWO 0
+#endif
 __device__ __forceinline__ void cfma_row(double2 (&acc)[TB], double2 av, const double2 (&w)[TB], const int RHO) {
   if (!LHAF_TWOPASS) {
 #pragma unroll
@@ -527,6 +530,26 @@ __device__ __forceinline__ void rs_op(double2 (&acc)[LM], const double2 *__restr
 #endif
 }
 
+// acc[t] += sum_{s + q = t} av(s) B[q] with av(s) = (a1 + b1 s) p1[max(s - o1, 0)] + (a2 + b2 s) p2[max(s - o2, 0)]
+// (operands in shared memory): one code instance serves the plain products (a1 = 1, the rest 0)
+// and t log D = sum_s (s D_s) R_{t-s} with s D_s = s (-2 w Kab[s-1] + w^2 Delta[s-2]) rebuilt from
+// the staged series (tree_pivot_s: two unrolled triangular routines instead of three).
+template <int LM>
+__device__ __forceinline__ void rs_op2(double2 (&acc)[LM], const double2 *p1, int o1, double a1, double b1,
+                                       const double2 *p2, int o2, double a2, double b2,
+                                       const double2 (&B)[LM], int L) {
+#pragma unroll
+  for (int s = 0; s < LM; ++s) {
+    if (s < L) {
+      const double c1 = fma(b1, (double)s, a1), c2 = fma(b2, (double)s, a2);
+      const double2 v1 = p1[max(s - o1, 0)], v2 = p2[max(s - o2, 0)];
+      const double2 av = make_double2(fma(c2, v2.x, c1 * v1.x), fma(c2, v2.y, c1 * v1.y));
+#pragma unroll
+      for (int q = 0; q + s < LM; ++q) acc[q + s] = cfma(av, B[q], acc[q + s]);
+    }
+  }
+}
+
 // ================================================================ kernels
 struct TStep {  // parent depth k -> children at depth k + 1, one chunk of children
   TLevel par, ch;
@@ -663,6 +686,65 @@ __global__ void __launch_bounds__(PV_THREADS, 2) tree_pivot_s(TStep P) {
   const int pl = (int)(ps - psf);
   const double wd = (double)w, w2 = wd * wd;
   double2 A[LM], B[LM];
+#if LHAF_PIVOT_TWO
+  const bool live = active && w != 0;
+  if (live) {
+    rdet(A, bKab + pl * SP, bX + pl * SP, w, L);                // A = D_w
+    rrec(B, A, L, 1.0, 0.0, -1.0, false);                     // B = 1/D
+  } else if (active) {  // deleted pair: D = 1, Q = 0
+    const double2 *lp = P.par.logc + (int64_t)ps * L;
+    double2 *lc = P.ch.logc + (int64_t)i * L, *Q = P.Q + (int64_t)i * 3 * L;
+    for (int t = 0; t < L; ++t) { lc[t] = lp[t]; Q[t] = Q[L + t] = Q[2 * L + t] = c0(); }
+  }
+  if (active) P.ch.coef[i] = P.par.coef[ps] * ((kh & 1) ? -1.0 : 1.0) * binom_d(P.eta, kh);
+  double2 *Q = P.Q + (int64_t)i * 3 * L;
+  // qi = 0: A = t log D = sum_s (s D_s) R_{t-s};  qi = 1..3: lam K R for K = Kbb, Kaa, Kab
+#pragma unroll 1
+  for (int qi = 0; qi < 4; ++qi) {
+    if (live) {
+      rz(A);
+      const double2 *p1 = (qi == 0 ? bKab : qi == 1 ? bX : qi == 2 ? bKaa : bKab) + pl * SP;
+      const double2 *p2 = (qi == 0 ? bX : p1) + (qi == 0 ? pl * SP : 0);
+      // s D_s = s (-2 w Kab[s-1] + w^2 Delta[s-2]): the clamped index at s < offset meets a zero
+      // coefficient for s = 0 only; s = 1 of the Delta term must vanish too: D_1 has no Delta part
+      rs_op2(A, p1, qi == 0 ? 1 : 0, qi == 0 ? 0.0 : 1.0, qi == 0 ? -2.0 * wd : 0.0,
+             p2, qi == 0 ? 2 : 0, 0.0, qi == 0 ? w2 : 0.0, B, L);
+      if (qi == 0) {
+        // the s = 1 step took Delta[max(1 - 2, 0)] = Delta[0] with coefficient w^2: remove it
+        const double2 d0 = (bX + pl * SP)[0];
+        const double2 av = make_double2(-w2 * d0.x, -w2 * d0.y);
+#pragma unroll
+        for (int q = 0; q + 1 < LM; ++q) A[q + 1] = cfma(av, B[q], A[q + 1]);
+        const double2 *lp = P.par.logc + (int64_t)ps * L;
+        double2 *lc = P.ch.logc + (int64_t)i * L;
+#pragma unroll
+        for (int t = 0; t < LM; ++t)
+          if (t < L) lc[t] = t ? cadd(lp[t], cscale(A[t], 1.0 / t)) : lp[t];
+      } else {
+#pragma unroll
+        for (int t = 0; t < LM; ++t) {
+          if (t < L) {
+            const double2 m = t ? A[t - 1] : c0();
+            if (qi == 1) Q[t] = cscale(m, w2);                                           // q11
+            else if (qi == 2) Q[2 * L + t] = cscale(m, w2);                              // q22
+            else Q[L + t] = make_double2(wd * B[t].x - w2 * m.x, wd * B[t].y - w2 * m.y);  // q12
+          }
+        }
+      }
+    }
+    if (qi == 0) {
+      __syncthreads();  // Delta consumed: K_bb takes its buffer
+      for (int c = threadIdx.x; c < NP * L; c += PV_THREADS) {
+        const int p = c / L, sx = c - p * L;
+        cp_async16(bX + p * SP + sx, P.par.K + ((int64_t)(psf + p) * NE + tri(b, b)) * L + sx);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+    }
+  }
+}
+#else
+  double2 A[LM], B[LM];
   if (active && w != 0) {
     rdet(A, bKab + pl * SP, bX + pl * SP, w, L);                // A = D_w
     rrec(B, A, L, 1.0, 0.0, -1.0, false);                     // B = 1/D
@@ -702,6 +784,7 @@ __global__ void __launch_bounds__(PV_THREADS, 2) tree_pivot_s(TStep P) {
     }
   }
 }
+#endif
 
 // generic pivot (any L): the blocked series routines above with per-child scratch in HBM
 __global__ void __launch_bounds__(128) tree_pivot_g(TStep P) {
