@@ -744,7 +744,6 @@ __global__ void __launch_bounds__(PV_THREADS, 2) tree_pivot_s(TStep P) {
   }
 }
 #else
-  double2 A[LM], B[LM];
   if (active && w != 0) {
     rdet(A, bKab + pl * SP, bX + pl * SP, w, L);                // A = D_w
     rrec(B, A, L, 1.0, 0.0, -1.0, false);                     // B = 1/D
