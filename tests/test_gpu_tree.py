@@ -51,6 +51,19 @@ def test_tree_random_collisions(tree, orc, seed):
     check(got, ref, sabs)
 
 
+@pytest.mark.parametrize("N", list(range(2, 29, 2)) + [7, 13, 21])
+def test_tree_series_length_sweep(tree, orc, N):
+    # distinct modes, n = ceil(N / 2) pairs, series length L = n + 1 = 2 .. 15: every remainder
+    # of tree_bc_k's product routine (chunks of TB = 8 steps + a tail of L mod 8, the block
+    # triangle with fewer than TB - 1 operands when L < 8) and odd N (phantom index)
+    rng = G.rng_for(7300 + N)
+    A = G.pure_B(G.haar_unitary(N, rng), 0.7)
+    g = G.complex_gaussian(N, 0.3, rng)
+    reps = [1] * N
+    ref, T, sabs = orc.lhaf_fds(A, g, reps)
+    check(tree.lhaf_rpt(A, g, reps), ref, sabs, tol=1e-10 if N <= 24 else 1e-8)  # north_star tolerances
+
+
 @pytest.mark.parametrize("reps", [[1], [2], [3], [4], [6], [2, 2], [4, 2], [2, 2, 2], [1, 1], [5, 1]])
 def test_tree_single_and_even(tree, orc, reps):
     # one pair (the root is the leaf level), self-pairs, and all-even multiplicities (every eta
